@@ -1,0 +1,862 @@
+// dgt.cu -- plan, window preparation, the Zak/factorisation kernels and the C ABI.
+//
+// The method:
+//   Algorithm 1 of PAPER.md:852-900 reduces the nonseparable lattice (a, M, lambda)
+//   to a separable one by the chirp P_{s1} (time shear) or by a length-L FFT and the
+//   chirp P_{-s0} (frequency shear, with the Fourier-domain trick PAPER.md:902-919).
+//   The separable DGT with a full-length window is the factorisation algorithm whose
+//   cost is Eq. (rect-flops): Zak gather + d-point DFTs, p x q
+//   products against the window factorisation, d-point DFTs, M-point FFTs.  The final
+//   phase and index remap of Alg. 1 (lines 9-15 / 25-31) is fused into the store.
+//
+// Kernel A (zak_kernel):   one CTA = (signal w, residue block r0..r0+RB, l).  Gathers
+//   f~(x(r,k,l,s)) with the chirp multiplied on load, DFT_d over s, products with the
+//   plan's window factors, DFT_d over nu, and writes the intermediate C[w][j'][kappa][n'].
+// Kernel B (out_kernel):   one CTA = (signal w, tile of consecutive n).  Reads the
+//   columns C(., n), FFT over j, then the Alg. 1 phase + remap, and stores c[w][m][n].
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/nsdgt.h"
+#include "cplx.cuh"
+#include "fft_smem.cuh"
+#include "planner.hpp"
+#include "fast_kernels.cuh"
+
+namespace nsdgt {
+
+static thread_local std::string g_last_error;
+static thread_local int64_t g_last_lmin = 0;
+
+static int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return fail(_e == cudaErrorMemoryAllocation ? DGT_ENOMEM : DGT_ECUDA,           \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                \
+    } while (0)
+
+#define CUFFT_TRY(expr)                                                                     \
+    do {                                                                                    \
+        cufftResult _r = (expr);                                                            \
+        if (_r != CUFFT_SUCCESS)                                                            \
+            return fail(_r == CUFFT_ALLOC_FAILED ? DGT_ENOMEM : DGT_ECUFFT,                 \
+                        std::string(#expr) + ": cufft status " + std::to_string((int)_r));  \
+    } while (0)
+
+// ---------------------------------------------------------------------------------
+// plan-time device kernels (fp64 arithmetic, cast once to the working precision)
+// ---------------------------------------------------------------------------------
+
+// P_sigma(x) = exp(i pi r / L), r = (sigma * x^2 * (L+1)) mod 2L  (
+// reading Z4: every factor reduced mod 2L first, exact in 128-bit integers).
+__device__ __forceinline__ double2 chirp_val(int64_t sigma, int64_t x, int64_t L) {
+    const unsigned __int128 twoL = (unsigned __int128)(2 * L);
+    const unsigned __int128 sg = (unsigned __int128)(((sigma % (2 * L)) + 2 * L) % (2 * L));
+    const unsigned __int128 xx = ((unsigned __int128)x * (unsigned __int128)x) % twoL;
+    const unsigned __int128 lp = (unsigned __int128)((L + 1) % (2 * L));
+    const unsigned __int128 r = (sg * xx % twoL) * lp % twoL;
+    double s, c;
+    sincospi((double)(int64_t)r / (double)L, &s, &c);
+    return make_double2(c, s);
+}
+
+template <typename T>
+__global__ void k_chirp_table(cx<T>* out, int64_t sigma, int64_t L) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < L; x += (int64_t)gridDim.x * blockDim.x) {
+        double2 v = chirp_val(sigma, x, L);
+        out[x] = mk<T>((T)v.x, (T)v.y);
+    }
+}
+
+// gt = P_sigma * g  (fp64), g given in precision Tin
+template <typename Tin>
+__global__ void k_window_time(double2* gt, const cx<Tin>* g, int64_t sigma, int64_t L) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < L; x += (int64_t)gridDim.x * blockDim.x) {
+        double2 gv = make_double2((double)g[x].x, (double)g[x].y);
+        double2 v = sigma ? cmul(chirp_val(sigma, x, L), gv) : gv;
+        gt[x] = v;
+    }
+}
+
+// after the fp64 FFT: ghat = P_{-s0} * FFT(P_{s1} g) / L   (Alg. 1 line 22)
+__global__ void k_window_freq_post(double2* gh, int64_t sigma, int64_t L) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < L; x += (int64_t)gridDim.x * blockDim.x) {
+        double2 v = cmul(chirp_val(sigma, x, L), gh[x]);
+        gh[x] = make_double2(v.x / (double)L, v.y / (double)L);
+    }
+}
+
+// Window factorisation: for r<c, u<q, k<p, nu<d
+//   Gamma_r(k,u;nu) = sum_{s<d} g~(x(r,k,u,s)) exp(-2 pi i s nu / d),
+//   x(r,k,u,s) = r + c ((k q + p u + s p q) mod (L/c)),
+// stored as G[((r*q + u)*p + k)*d + nu] = conj(Gamma)/d.  Direct sum in fp64 with exact
+// integer reduction of s*nu mod d (plan time only).
+template <typename T>
+__global__ void k_window_factor(cx<T>* G, const double2* gt, int64_t L, int64_t c, int64_t d, int64_t p,
+                                int64_t q) {
+    const int64_t total = c * q * p * d;
+    const int64_t Lc = L / c;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t nu = i % d;
+        const int64_t k = (i / d) % p;
+        const int64_t u = (i / (d * p)) % q;
+        const int64_t r = i / (d * p * q);
+        double sr = 0.0, si = 0.0;
+        int64_t e = 0;  // s*nu mod d
+        for (int64_t s = 0; s < d; ++s) {
+            const int64_t x = r + c * ((k * q + p * u + s * p * q) % Lc);
+            double sn, cs;
+            sincospi(-2.0 * (double)e / (double)d, &sn, &cs);
+            const double2 gv = gt[x];
+            sr += gv.x * cs - gv.y * sn;
+            si += gv.x * sn + gv.y * cs;
+            e += nu;
+            if (e >= d) e -= d;
+        }
+        G[i] = mk<T>((T)(sr / (double)d), (T)(-si / (double)d));
+    }
+}
+
+template <typename T>
+__global__ void k_twiddles(cx<T>* tw, int64_t n) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        double s, c;
+        sincospi(-2.0 * (double)k / (double)n, &s, &c);
+        tw[k] = mk<T>((T)c, (T)s);
+    }
+}
+
+// T-branch post tables (Alg. 1 lines 8-12): E(n) = exp(i pi (C1 n^2 mod 2N)/N) and the
+// row rotation rot(n) = ceil(s1 a n / b) mod M (the printed ((-s1 n a + m b) mod L) div b
+// equals (m - rot(n)) mod M; reading Z5).
+template <typename T>
+__global__ void k_post_time(cx<T>* E, int* rot, int64_t N, int64_t C1, int64_t s1, int64_t a, int64_t b,
+                            int64_t M) {
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned __int128 twoN = 2 * N;
+        const int64_t e = (int64_t)(((unsigned __int128)C1 * (((unsigned __int128)n * n) % twoN)) % twoN);
+        double s, c;
+        sincospi((double)e / (double)N, &s, &c);
+        E[n] = mk<T>((T)c, (T)s);
+        const __int128 x = (__int128)s1 * a * n;
+        rot[n] = (int)(((x + b - 1) / b) % M);
+    }
+}
+
+// F-branch phase table ptab[e] = exp(i pi e / N), e < 2N.
+template <typename T>
+__global__ void k_phase_table(cx<T>* P, int64_t N) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 2 * N; e += (int64_t)gridDim.x * blockDim.x) {
+        double s, c;
+        sincospi((double)e / (double)N, &s, &c);
+        P[e] = mk<T>((T)c, (T)s);
+    }
+}
+
+template <typename T>
+__global__ void k_cast_to(cx<T>* out, const double2* in, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = mk<T>((T)in[i].x, (T)in[i].y);
+}
+
+// ---------------------------------------------------------------------------------
+// execute-time kernels (generic path)
+// ---------------------------------------------------------------------------------
+
+// F-branch front end: out = P_pre(x) * f(x) (promotes real input), written complex.
+template <typename T>
+__global__ void k_prechirp(cx<T>* out, const void* f, int real_in, const cx<T>* __restrict__ chirp, int64_t L,
+                           int64_t total) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        cx<T> v;
+        if (real_in) v = mk<T>(((const T*)f)[i], T(0));
+        else v = ((const cx<T>*)f)[i];
+        if (chirp) v = cmul(v, chirp[i % L]);
+        out[i] = v;
+    }
+}
+
+struct ZakArgs {
+    const void* f;     // [W][L] complex (or real) input of the inner separable DGT
+    int real_in;
+    const void* chirp;  // [L] multiplier applied on load (nullable)
+    const void* G;      // window factors [c][q][p][d]
+    void* C;            // intermediate [W][iM][q][d]
+    int64_t L, c, d, p, q, iM;
+    int RB;
+    Radices rd;
+    const void* tw;     // twiddles of length d
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using C = cx<T>;
+    const int64_t d = A.d, p = A.p, q = A.q, c = A.c, L = A.L;
+    const int RB = A.RB;
+    const int nrb = (int)((c + RB - 1) / RB);
+    const int rblk = blockIdx.x % nrb;
+    const int l = blockIdx.x / nrb;
+    const int64_t w = blockIdx.y;
+    const int64_t r0 = (int64_t)rblk * RB;
+    const int nr = (int)((c - r0) < RB ? (c - r0) : RB);
+    C* bufA = (C*)smem_raw;                 // RB*p*d
+    C* bufB = bufA + (size_t)RB * p * d;    // RB*p*d (>= RB*d)
+    C* bufY = bufB + (size_t)RB * p * d;    // RB*d
+    const C* __restrict__ tw = (const C*)A.tw;
+    const C* __restrict__ chirp = (const C*)A.chirp;
+    const int64_t Lc = L / c;
+
+    // 1. gather f~(x(r,k,l,s)), x = r + c((k q + p l + s p q) mod (L/c)), rr fastest
+    const int64_t ng = (int64_t)nr * p * d;
+    for (int64_t i = threadIdx.x; i < ng; i += blockDim.x) {
+        const int rr = (int)(i % nr);
+        const int64_t ks = i / nr;  // k*d + s
+        const int64_t s = ks % d, k = ks / d;
+        const int64_t x = r0 + rr + c * ((k * q + p * l + s * p * q) % Lc);
+        C v;
+        if (A.real_in) v = mk<T>(((const T*)A.f)[w * L + x], T(0));
+        else v = ((const C*)A.f)[w * L + x];
+        if (chirp) v = cmul(v, chirp[x]);
+        bufA[(rr * p + k) * d + s] = v;
+    }
+    __syncthreads();
+    // 2. DFT_d over s for nr*p sequences
+    C* phi = fft_smem<T>(bufA, bufB, A.rd, nr * (int)p, (int)d, tw);
+    C* free0 = (phi == bufA) ? bufB : bufA;
+    const C* __restrict__ G = (const C*)A.G;
+    C* Cout = (C*)A.C;
+    const int64_t jp = (l * p) % q;  // j' = r + c*((l p) mod q)
+    for (int u = 0; u < q; ++u) {
+        // 3. Y(nu) = sum_k Phi_r(k,l;nu) * conj(Gamma_r(k,u;nu))/d
+        for (int64_t i = threadIdx.x; i < (int64_t)nr * d; i += blockDim.x) {
+            const int rr = (int)(i / d);
+            const int64_t nu = i % d;
+            const C* gk = G + (((r0 + rr) * q + u) * p) * d + nu;
+            C acc = cmul(phi[(rr * p) * d + nu], gk[0]);
+            for (int64_t k = 1; k < p; ++k) acc = acc + cmul(phi[(rr * p + k) * d + nu], gk[k * d]);
+            free0[rr * d + nu] = acc;
+        }
+        __syncthreads();
+        // 4. DFT_d over nu
+        C* Y = fft_smem<T>(free0, bufY, A.rd, nr, (int)d, tw);
+        // 5. scatter T_r(l,u;tau) to n = (l - u - q tau) mod N:
+        //    kappa = (l-u) mod q, n' = (-tau - [l<u]) mod d, C[w][j'][kappa][n']
+        const int64_t kappa = ((l - u) % q + q) % q;
+        const int64_t off = (l < u) ? 1 : 0;
+        for (int64_t i = threadIdx.x; i < (int64_t)nr * d; i += blockDim.x) {
+            const int rr = (int)(i / d);
+            const int64_t np = i % d;                 // destination n'
+            const int64_t tau = ((-np - off) % d + d) % d;
+            const int64_t j = r0 + rr + c * jp;
+            Cout[((w * A.iM + j) * q + kappa) * d + np] = Y[rr * d + tau];
+        }
+        __syncthreads();
+    }
+}
+
+struct OutArgs {
+    const void* C;  // [W][iM][q][d]
+    void* out;      // [W][M][N]
+    int64_t iM, iN, q, d;
+    int NT;         // columns (consecutive inner n) per CTA
+    Radices rd;
+    const void* tw;  // twiddles of length iM
+    int branch;
+    // T-branch
+    const void* E;
+    const int* rot;
+    int64_t M, N;
+    // F-branch
+    const void* ptab;
+    int64_t L, b, Nr, ar, s1, C1, C2, C3, C4, C5, C6;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using C = cx<T>;
+    const int64_t iM = A.iM, iN = A.iN, q = A.q, d = A.d;
+    const int NT = A.NT;
+    const int64_t n0 = (int64_t)blockIdx.x * NT;
+    const int nt = (int)((iN - n0) < NT ? (iN - n0) : NT);
+    const int64_t w = blockIdx.y;
+    C* bufA = (C*)smem_raw;
+    C* bufB = bufA + (size_t)NT * iM;
+    const C* __restrict__ Cin = (const C*)A.C + w * iM * iN;
+    // load columns n0..n0+nt: C(j, n) stored at [j][n mod q][n div q]
+    for (int64_t i = threadIdx.x; i < (int64_t)nt * iM; i += blockDim.x) {
+        const int cl = (int)(i % nt);
+        const int64_t j = i / nt;
+        const int64_t n = n0 + cl;
+        bufA[cl * iM + j] = Cin[(j * q + (n % q)) * d + n / q];
+    }
+    __syncthreads();
+    C* X = fft_smem<T>(bufA, bufB, A.rd, nt, (int)iM, (const C*)A.tw);
+    if (A.branch != DGT_BRANCH_FREQ) {
+        // c[w][(m - rot(n)) mod M][n] = E(n) * X(m, n)   (Alg. 1 lines 9-12)
+        C* out = (C*)A.out + w * A.M * A.N;
+        const C* E = (const C*)A.E;
+        for (int64_t i = threadIdx.x; i < (int64_t)nt * iM; i += blockDim.x) {
+            const int cl = (int)(i % nt);
+            const int64_t mo = i / nt;
+            const int64_t n = n0 + cl;
+            int64_t m = mo + A.rot[n];
+            if (m >= A.M) m -= A.M;
+            out[mo * A.N + n] = cmul(E[n], X[cl * iM + m]);
+        }
+    } else {
+        // c[kt][mt] = E(k,m) c_r[(-k) mod N_r][m]  (Alg. 1 lines 24-31); here the inner
+        // channel is the FFT output index kc = (-k) mod N_r, the inner time index m = n.
+        C* out = (C*)A.out + w * A.M * A.N;
+        const C* P = (const C*)A.ptab;
+        const int64_t twoN = 2 * A.N, Nn = A.N, L = A.L;
+        for (int64_t i = threadIdx.x; i < (int64_t)nt * iM; i += blockDim.x) {
+            const int64_t kc = i % iM;
+            const int cl = (int)(i / iM);
+            const int64_t m = n0 + cl;
+            const int64_t k = (A.Nr - kc) % A.Nr;
+            const int64_t sq = (A.C1 * k + A.C2 * (m % twoN)) % twoN;
+            const int64_t t1 = (A.C3 * ((sq * sq) % twoN)) % twoN;
+            const int64_t t2 = ((m % twoN) * ((A.C4 * (m % twoN) + A.C5 * k) % twoN)) % twoN;
+            const int64_t e = ((t1 - t2) % twoN + twoN) % twoN;
+            const int64_t mt = (A.C1 * k + A.C2 * (m % Nn)) % Nn;
+            const int64_t kt = ((((-(A.s1 % L) * ((A.ar * k) % L)) % L + (A.C6 * m) % L) % L + L) % L) / A.b;
+            out[kt * Nn + mt] = cmul(P[e], X[cl * iM + kc]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// the plan
+// ---------------------------------------------------------------------------------
+
+struct Plan {
+    dgt_lattice_info info{};
+    int dtype = DGT_C64;
+    int flags = 0;
+    int device = 0;
+    size_t esz = 8;  // complex element size
+    // device tables
+    void* G = nullptr;       // window factors (L complex)
+    void* chirp = nullptr;   // kernel-A load multiplier (L complex) or null
+    void* pre = nullptr;     // F-branch pre-FFT chirp (L complex) or null
+    void* tw_d = nullptr;    // twiddles length d
+    void* tw_m = nullptr;    // twiddles length iM
+    void* E = nullptr;       // T-branch column phases (N)
+    int* rot = nullptr;      // T-branch rotations (N)
+    void* ptab = nullptr;    // F-branch phase table (2N)
+    // workspace
+    void* Cws = nullptr;     // chunk intermediate
+    void* fhat = nullptr;    // F-branch chunk spectra
+    int64_t chunk = 1;
+    size_t ws_bytes = 0;
+    std::map<int64_t, cufftHandle> fft_plans;
+    // kernel configuration
+    Radices rd_d{}, rd_m{};
+    int RB = 1, NT = 1;
+    size_t smemA = 0, smemB = 0;
+    int fast = 0;  // specialised path id (0 = generic)
+    FastPlan fp{};
+    // host pipeline (dgt_execute_host)
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    void* stage_f[2] = {nullptr, nullptr};
+    void* stage_c[2] = {nullptr, nullptr};
+    int64_t stage_W = 0;
+    // profiling (dgt_profile_begin / dgt_profile_end)
+    struct ProfRec {
+        int kind;
+        cudaEvent_t a, b;
+        double bytes, flops;
+    };
+    bool prof = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t pool_used = 0;
+};
+
+enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_COUNT = 4 };
+static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast"};
+
+static cudaEvent_t prof_event(Plan* P) {
+    if (P->pool_used == P->pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        P->pool.push_back(e);
+    }
+    return P->pool[P->pool_used++];
+}
+// open a timed region on `st` (returns index or -1 when not profiling)
+static int prof_open(Plan* P, cudaStream_t st) {
+    if (!P->prof) return -1;
+    Plan::ProfRec r{};
+    r.a = prof_event(P);
+    r.b = prof_event(P);
+    cudaEventRecord(r.a, st);
+    P->recs.push_back(r);
+    return (int)P->recs.size() - 1;
+}
+static void prof_close(Plan* P, int h, int kind, double bytes, double flops, cudaStream_t st) {
+    if (h < 0) return;
+    Plan::ProfRec& r = P->recs[h];
+    r.kind = kind;
+    r.bytes = bytes;
+    r.flops = flops;
+    cudaEventRecord(r.b, st);
+}
+
+static void free_plan(Plan* P) {
+    if (!P) return;
+    void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
+                    P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1]};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    free_fast(&P->fp);
+    for (auto& kv : P->fft_plans) cufftDestroy(kv.second);
+    for (cudaEvent_t e : P->pool) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+        if (P->ev_in[i]) cudaEventDestroy(P->ev_in[i]);
+        if (P->ev_comp[i]) cudaEventDestroy(P->ev_comp[i]);
+        if (P->ev_out[i]) cudaEventDestroy(P->ev_out[i]);
+    }
+    if (P->s_in) cudaStreamDestroy(P->s_in);
+    if (P->s_out) cudaStreamDestroy(P->s_out);
+    delete P;
+}
+
+static int grid_for(int64_t n, int block = 256) {
+    int64_t g = (n + block - 1) / block;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 64));
+}
+
+static int get_fft_plan(Plan* P, int64_t batch, cudaStream_t st, cufftHandle* out) {
+    auto it = P->fft_plans.find(batch);
+    if (it == P->fft_plans.end()) {
+        cufftHandle h;
+        long long n = P->info.L;
+        size_t wsz = 0;
+        CUFFT_TRY(cufftCreate(&h));
+        CUFFT_TRY(cufftMakePlanMany64(h, 1, &n, nullptr, 1, n, nullptr, 1, n,
+                                      P->dtype == DGT_C64 ? CUFFT_C2C : CUFFT_Z2Z, (long long)batch, &wsz));
+        P->fft_plans[batch] = h;
+        it = P->fft_plans.find(batch);
+    }
+    CUFFT_TRY(cufftSetStream(it->second, st));
+    *out = it->second;
+    return DGT_OK;
+}
+
+template <typename T>
+static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st) {
+    using C = cx<T>;
+    const dgt_lattice_info& I = P->info;
+    const int64_t L = I.L;
+    // window in the caller's precision -> device
+    C* g_dev = nullptr;
+    CUDA_TRY(cudaMalloc(&g_dev, sizeof(C) * L));
+    CUDA_TRY(cudaMemcpyAsync(g_dev, g_in, sizeof(C) * L, g_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    double2* gt = nullptr;
+    CUDA_TRY(cudaMalloc(&gt, sizeof(double2) * L));
+    if (I.branch != DGT_BRANCH_FREQ) {
+        // Alg. 1 line 4: g~ = pchirp(L, s1) g
+        k_window_time<T><<<grid_for(L), 256, 0, st>>>(gt, g_dev, I.s1, L);
+    } else {
+        // Alg. 1 lines 4, 22: g^ = pchirp(L,-s0) fft(pchirp(L,s1) g) / L, in fp64
+        k_window_time<T><<<grid_for(L), 256, 0, st>>>(gt, g_dev, I.s1, L);
+        cufftHandle h;
+        CUFFT_TRY(cufftPlan1d(&h, (int)L, CUFFT_Z2Z, 1));
+        CUFFT_TRY(cufftSetStream(h, st));
+        CUFFT_TRY(cufftExecZ2Z(h, (cufftDoubleComplex*)gt, (cufftDoubleComplex*)gt, CUFFT_FORWARD));
+        k_window_freq_post<<<grid_for(L), 256, 0, st>>>(gt, -I.s0, L);
+        CUDA_TRY(cudaStreamSynchronize(st));
+        cufftDestroy(h);
+    }
+    CUDA_TRY(cudaMalloc(&P->G, sizeof(C) * L));
+    k_window_factor<T><<<grid_for(L), 256, 0, st>>>((C*)P->G, gt, L, I.c, I.d, I.p, I.q);
+    // chirp multiplied on kernel-A load: T-branch P_{s1}, F-branch P_{-s0}
+    if (I.chirp_sigma % (2 * L) != 0) {
+        CUDA_TRY(cudaMalloc(&P->chirp, sizeof(C) * L));
+        k_chirp_table<T><<<grid_for(L), 256, 0, st>>>((C*)P->chirp, I.chirp_sigma, L);
+    }
+    if (I.branch == DGT_BRANCH_FREQ && I.pre_sigma % (2 * L) != 0) {
+        CUDA_TRY(cudaMalloc(&P->pre, sizeof(C) * L));
+        k_chirp_table<T><<<grid_for(L), 256, 0, st>>>((C*)P->pre, I.pre_sigma, L);
+    }
+    CUDA_TRY(cudaMalloc(&P->tw_d, sizeof(C) * I.d));
+    k_twiddles<T><<<grid_for(I.d), 256, 0, st>>>((C*)P->tw_d, I.d);
+    CUDA_TRY(cudaMalloc(&P->tw_m, sizeof(C) * I.iM));
+    k_twiddles<T><<<grid_for(I.iM), 256, 0, st>>>((C*)P->tw_m, I.iM);
+    if (I.branch != DGT_BRANCH_FREQ) {
+        CUDA_TRY(cudaMalloc(&P->E, sizeof(C) * I.N));
+        CUDA_TRY(cudaMalloc(&P->rot, sizeof(int) * I.N));
+        k_post_time<T><<<grid_for(I.N), 256, 0, st>>>((C*)P->E, P->rot, I.N, I.C1, I.s1, I.a, I.b, I.M);
+    } else {
+        CUDA_TRY(cudaMalloc(&P->ptab, sizeof(C) * 2 * I.N));
+        k_phase_table<T><<<grid_for(2 * I.N), 256, 0, st>>>((C*)P->ptab, I.N);
+    }
+    CUDA_TRY(cudaGetLastError());
+    int rc = build_fast<T>(&P->fp, P->info, P->G, P->chirp, P->E, P->rot, (P->flags & DGT_FORCE_GENERIC) != 0, st);
+    if (rc) return rc;
+    P->fast = P->fp.kind;
+    CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(g_dev);
+    cudaFree(gt);
+    return DGT_OK;
+}
+
+template <typename T>
+static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_t st) {
+    using C = cx<T>;
+    const dgt_lattice_info& I = P->info;
+    const bool real_in = (P->flags & DGT_REAL_INPUT) != 0;
+    const void* src = f;
+    int real_src = real_in ? 1 : 0;
+    const double e = (double)sizeof(C), ein = real_in ? e / 2 : e;
+    const double L = (double)I.L, MN = (double)I.M * (double)I.N;
+    const double lg_d = std::log2((double)I.d), lg_m = std::log2((double)I.iM);
+    if (I.branch == DGT_BRANCH_FREQ) {
+        const int ph = prof_open(P, st);
+        // Alg. 1 line 23: f^ = fft(pchirp(L, s1) f) (unnormalised), then P_{-s0} on load
+        cufftHandle h;
+        int rc = get_fft_plan(P, Wc, st, &h);
+        if (rc) return rc;
+        const void* fin = f;
+        if (real_in || P->pre) {
+            k_prechirp<T><<<grid_for(Wc * I.L), 256, 0, st>>>((C*)P->fhat, f, real_in ? 1 : 0, (const C*)P->pre,
+                                                              I.L, Wc * I.L);
+            fin = P->fhat;
+        }
+        if (P->dtype == DGT_C64)
+            CUFFT_TRY(cufftExecC2C(h, (cufftComplex*)fin, (cufftComplex*)P->fhat, CUFFT_FORWARD));
+        else
+            CUFFT_TRY(cufftExecZ2Z(h, (cufftDoubleComplex*)fin, (cufftDoubleComplex*)P->fhat, CUFFT_FORWARD));
+        src = P->fhat;
+        real_src = 0;
+        // Table 1 "Freq. shear": one length-L FFT of f per signal (4 L log2 L)
+        prof_close(P, ph, PK_FRONT, Wc * L * ein, Wc * 4.0 * L * std::log2(L), st);
+    }
+    // Eq. (rect-flops): 8Lq + 4L log2 d + 4MN log2 d + 4MN log2 M, plus 6MN for the phase
+    const double fl_zak = Wc * (8.0 * L * I.q / I.p + 4.0 * L * lg_d + 4.0 * MN * lg_d);
+    const double fl_out = Wc * (4.0 * MN * lg_m + 6.0 * MN);
+    const double by_in = (I.branch == DGT_BRANCH_FREQ ? 0.0 : Wc * L * ein) + L * e;  // f (T) + window factors
+    const double by_out = Wc * MN * e;
+    if (P->fast) {
+        const int ph = prof_open(P, st);
+        int rc = launch_fast<T>(&P->fp, src, real_src, P->Cws, c, Wc, st);
+        if (rc) return rc;
+        prof_close(P, ph, PK_FAST, by_in + by_out, fl_zak + fl_out, st);
+        CUDA_TRY(cudaGetLastError());
+        return DGT_OK;
+    }
+    ZakArgs A{};
+    A.f = src; A.real_in = real_src; A.chirp = P->chirp; A.G = P->G; A.C = P->Cws;
+    A.L = I.L; A.c = I.c; A.d = I.d; A.p = I.p; A.q = I.q; A.iM = I.iM;
+    A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d;
+    const int nrb = (int)((I.c + P->RB - 1) / P->RB);
+    int ph = prof_open(P, st);
+    zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+    prof_close(P, ph, PK_ZAK, by_in, fl_zak, st);
+    OutArgs B{};
+    B.C = P->Cws; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
+    B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
+    B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
+    B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
+    B.C1 = I.C1; B.C2 = I.C2; B.C3 = I.C3; B.C4 = I.C4; B.C5 = I.C5; B.C6 = I.C6;
+    const int ntiles = (int)((I.iN + P->NT - 1) / P->NT);
+    ph = prof_open(P, st);
+    out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
+    prof_close(P, ph, PK_OUT, by_out, fl_out, st);
+    CUDA_TRY(cudaGetLastError());
+    return DGT_OK;
+}
+
+template <typename T>
+static int configure(Plan* P, int64_t max_chunk) {
+    const dgt_lattice_info& I = P->info;
+    const size_t e = sizeof(cx<T>);
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    int smem_optin = 0, l2 = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    const size_t budget = std::min<size_t>((size_t)smem_optin, 200 * 1024);
+    if (I.d > (1 << 30) || I.iM > (1 << 30)) return fail(DGT_EUNSUPPORTED, "inner length too large");
+    P->rd_d = make_radices((int)I.d);
+    P->rd_m = make_radices((int)I.iM);
+    if (P->rd_d.nst > kMaxStages || P->rd_m.nst > kMaxStages) return fail(DGT_EUNSUPPORTED, "too many FFT stages");
+    // kernel A: residues per CTA for >= 32-byte gathers, within the smem budget
+    auto smemA = [&](int rb) { return (size_t)rb * (2 * I.p + 1) * I.d * e; };
+    int rb = (int)std::min<int64_t>(I.c, std::max<int64_t>(1, 64 / (int64_t)e));
+    while (rb > 1 && smemA(rb) > budget) --rb;
+    if (smemA(rb) > budget)
+        return fail(DGT_EUNSUPPORTED, "inner Zak length d=" + std::to_string(I.d) + " too large for shared memory");
+    P->RB = rb;
+    P->smemA = smemA(rb);
+    auto smemB = [&](int nt) { return (size_t)2 * nt * I.iM * e; };
+    int nt = (int)std::min<int64_t>(I.iN, 16);
+    while (nt > 1 && smemB(nt) > budget) --nt;
+    if (smemB(nt) > budget)
+        return fail(DGT_EUNSUPPORTED, "inner channel count " + std::to_string(I.iM) + " too large for shared memory");
+    P->NT = nt;
+    P->smemB = smemB(nt);
+    CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+    CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
+    // chunk: intermediate of a chunk stays well inside L2
+    const size_t per_sig = (size_t)I.iM * I.iN * e;
+    int64_t ch = std::max<int64_t>(1, (int64_t)((size_t)(l2 > 0 ? l2 : (64 << 20)) * 2 / 5 / per_sig));
+    if (max_chunk > 0) ch = max_chunk;
+    P->chunk = ch;
+    return DGT_OK;
+}
+
+static int alloc_workspace(Plan* P, int64_t Wc) {
+    const dgt_lattice_info& I = P->info;
+    if (P->Cws) return DGT_OK;
+    size_t need = (size_t)Wc * I.iM * I.iN * P->esz;
+    if (P->fast) need = std::max(need, fast_workspace_bytes(&P->fp, Wc));
+    CUDA_TRY(cudaMalloc(&P->Cws, need));
+    P->ws_bytes = need;
+    if (I.branch == DGT_BRANCH_FREQ) {
+        CUDA_TRY(cudaMalloc(&P->fhat, (size_t)Wc * I.L * P->esz));
+        P->ws_bytes += (size_t)Wc * I.L * P->esz;
+    }
+    return DGT_OK;
+}
+
+static int execute(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) {
+    const dgt_lattice_info& I = P->info;
+    const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
+    for (int64_t w0 = 0; w0 < W; w0 += P->chunk) {
+        const int64_t wc = std::min<int64_t>(P->chunk, W - w0);
+        const void* fc = (const char*)f + (size_t)w0 * I.L * ein;
+        void* cc = (char*)c + (size_t)w0 * I.M * I.N * P->esz;
+        int rc = P->dtype == DGT_C64 ? launch_chunk<float>(P, fc, cc, wc, st) : launch_chunk<double>(P, fc, cc, wc, st);
+        if (rc) return rc;
+    }
+    return DGT_OK;
+}
+
+}  // namespace nsdgt
+
+using namespace nsdgt;
+
+extern "C" {
+
+const char* dgt_version(void) { return "nsdgt 0.1 (sm_100a)"; }
+
+const char* dgt_strerror(int status) {
+    switch (status) {
+        case DGT_OK: return "ok";
+        case DGT_EINVAL: return "invalid argument";
+        case DGT_EILLEGAL_LENGTH: return "illegal transform length (L must be a multiple of L_min)";
+        case DGT_ECUDA: return "CUDA runtime error";
+        case DGT_ECUFFT: return "cuFFT error";
+        case DGT_ENOMEM: return "out of memory";
+        case DGT_EUNSUPPORTED: return "unsupported inner transform size";
+        default: return "unknown status";
+    }
+}
+
+const char* dgt_last_error(void) { return g_last_error.c_str(); }
+int64_t dgt_last_lmin(void) { return g_last_lmin; }
+
+int dgt_lattice_plan(int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, int flags, int force_shear,
+                     int64_t s0, int64_t s1, dgt_lattice_info* out) {
+    std::string err;
+    if (!out) return fail(DGT_EINVAL, "null output");
+    int rc = plan_lattice(L, a, M, l1, l2, flags, force_shear != 0, s0, s1, out, &err);
+    if (rc == DGT_EILLEGAL_LENGTH) g_last_lmin = out->L_min;
+    if (rc) return fail(rc, err);
+    return DGT_OK;
+}
+
+int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int dtype,
+             int flags, int64_t max_chunk, int force_shear, int64_t s0, int64_t s1, void* cuda_stream) {
+    if (!out || !g) return fail(DGT_EINVAL, "null pointer");
+    *out = nullptr;
+    if (dtype != DGT_C64 && dtype != DGT_C128) return fail(DGT_EINVAL, "bad dtype");
+    if (flags & ~(DGT_REAL_INPUT | DGT_G_ON_HOST | DGT_SHEAR_PAPER | DGT_FORCE_GENERIC))
+        return fail(DGT_EINVAL, "bad flags");
+    if (max_chunk < 0) return fail(DGT_EINVAL, "max_chunk < 0");
+    Plan* P = new Plan();
+    std::string err;
+    int rc = plan_lattice(L, a, M, l1, l2, flags, force_shear != 0, s0, s1, &P->info, &err);
+    if (rc) {
+        if (rc == DGT_EILLEGAL_LENGTH) g_last_lmin = P->info.L_min;
+        delete P;
+        return fail(rc, err);
+    }
+    P->dtype = dtype;
+    P->flags = flags;
+    P->esz = dtype == DGT_C64 ? 8 : 16;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    cudaGetDevice(&P->device);
+    rc = dtype == DGT_C64 ? configure<float>(P, max_chunk) : configure<double>(P, max_chunk);
+    if (!rc) rc = dtype == DGT_C64 ? build_tables<float>(P, g, (flags & DGT_G_ON_HOST) != 0, st)
+                                   : build_tables<double>(P, g, (flags & DGT_G_ON_HOST) != 0, st);
+    if (!rc && P->fast) {
+        P->chunk = max_chunk > 0 ? max_chunk : fast_chunk(&P->fp);
+    }
+    if (!rc) rc = alloc_workspace(P, P->chunk);
+    if (rc) {
+        free_plan(P);
+        return rc;
+    }
+    P->info.chunk = P->chunk;
+    P->info.workspace_bytes = (int64_t)P->ws_bytes;
+    P->info.kernel_path = P->fast;
+    *out = (dgt_plan_t)P;
+    return DGT_OK;
+}
+
+int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_stream) {
+    Plan* P = (Plan*)plan;
+    if (!P) return fail(DGT_EINVAL, "null plan");
+    if (W < 0) return fail(DGT_EINVAL, "W < 0");
+    if (W == 0) return DGT_OK;
+    if (!f || !c) return fail(DGT_EINVAL, "null pointer");
+    const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
+    const char* fb = (const char*)f;
+    const char* cb = (const char*)c;
+    const size_t fbytes = (size_t)W * P->info.L * ein, cbytes = (size_t)W * P->info.M * P->info.N * P->esz;
+    if (fb < cb + cbytes && cb < fb + fbytes) return fail(DGT_EINVAL, "f and c alias");
+    return execute(P, f, c, W, (cudaStream_t)cuda_stream);
+}
+
+int dgt_execute_host(dgt_plan_t plan, const void* f_host, void* c_host, int64_t W, void* cuda_stream) {
+    Plan* P = (Plan*)plan;
+    if (!P) return fail(DGT_EINVAL, "null plan");
+    if (W < 0) return fail(DGT_EINVAL, "W < 0");
+    if (W == 0) return DGT_OK;
+    if (!f_host || !c_host) return fail(DGT_EINVAL, "null pointer");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const dgt_lattice_info& I = P->info;
+    const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
+    const size_t per_f = (size_t)I.L * ein, per_c = (size_t)I.M * I.N * P->esz;
+    // staging chunk: a multiple of the compute chunk, ~256 MB of output per slot
+    int64_t sw = std::max<int64_t>(1, (int64_t)((256ull << 20) / per_c));
+    sw = std::max<int64_t>(P->chunk, sw / P->chunk * P->chunk);
+    sw = std::min<int64_t>(sw, W);
+    if (!P->s_in) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CUDA_TRY(cudaEventCreateWithFlags(&P->ev_in[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&P->ev_comp[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&P->ev_out[i], cudaEventDisableTiming));
+        }
+    }
+    if (P->stage_W < sw) {
+        for (int i = 0; i < 2; ++i) {
+            if (P->stage_f[i]) cudaFree(P->stage_f[i]);
+            if (P->stage_c[i]) cudaFree(P->stage_c[i]);
+            P->stage_f[i] = P->stage_c[i] = nullptr;
+        }
+        P->stage_W = 0;
+        for (int i = 0; i < 2; ++i) {
+            CUDA_TRY(cudaMalloc(&P->stage_f[i], per_f * sw));
+            CUDA_TRY(cudaMalloc(&P->stage_c[i], per_c * sw));
+        }
+        P->stage_W = sw;
+    }
+    // the caller's stream must be ordered before our copies start
+    CUDA_TRY(cudaEventRecord(P->ev_out[0], st));
+    CUDA_TRY(cudaStreamWaitEvent(P->s_in, P->ev_out[0], 0));
+    CUDA_TRY(cudaEventRecord(P->ev_out[1], st));
+    int64_t i = 0;
+    for (int64_t w0 = 0; w0 < W; w0 += sw, ++i) {
+        const int slot = (int)(i & 1);
+        const int64_t wc = std::min<int64_t>(sw, W - w0);
+        CUDA_TRY(cudaStreamWaitEvent(P->s_in, P->ev_out[slot], 0));
+        CUDA_TRY(cudaMemcpyAsync(P->stage_f[slot], (const char*)f_host + w0 * per_f, wc * per_f,
+                                 cudaMemcpyHostToDevice, P->s_in));
+        CUDA_TRY(cudaEventRecord(P->ev_in[slot], P->s_in));
+        CUDA_TRY(cudaStreamWaitEvent(st, P->ev_in[slot], 0));
+        int rc = execute(P, P->stage_f[slot], P->stage_c[slot], wc, st);
+        if (rc) return rc;
+        CUDA_TRY(cudaEventRecord(P->ev_comp[slot], st));
+        CUDA_TRY(cudaStreamWaitEvent(P->s_out, P->ev_comp[slot], 0));
+        CUDA_TRY(cudaMemcpyAsync((char*)c_host + w0 * per_c, P->stage_c[slot], wc * per_c, cudaMemcpyDeviceToHost,
+                                 P->s_out));
+        CUDA_TRY(cudaEventRecord(P->ev_out[slot], P->s_out));
+    }
+    CUDA_TRY(cudaStreamSynchronize(P->s_out));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return DGT_OK;
+}
+
+int dgt_destroy(dgt_plan_t plan) {
+    free_plan((Plan*)plan);
+    return DGT_OK;
+}
+
+int dgt_plan_query(dgt_plan_t plan, dgt_lattice_info* info) {
+    if (!plan || !info) return fail(DGT_EINVAL, "null pointer");
+    *info = ((Plan*)plan)->info;
+    return DGT_OK;
+}
+
+int dgt_profile_begin(dgt_plan_t plan) {
+    Plan* P = (Plan*)plan;
+    if (!P) return fail(DGT_EINVAL, "null plan");
+    P->prof = true;
+    P->recs.clear();
+    P->pool_used = 0;
+    return DGT_OK;
+}
+
+int dgt_profile_end(dgt_plan_t plan, dgt_kernel_stat* stats, int max_stats, int* n_stats) {
+    Plan* P = (Plan*)plan;
+    if (!P || (!stats && max_stats > 0) || !n_stats) return fail(DGT_EINVAL, "null pointer");
+    P->prof = false;
+    dgt_kernel_stat acc[PK_COUNT];
+    std::memset(acc, 0, sizeof acc);
+    for (auto& r : P->recs) {
+        CUDA_TRY(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+        acc[r.kind].launches += 1;
+        acc[r.kind].ms += ms;
+        acc[r.kind].bytes += r.bytes;
+        acc[r.kind].flops += r.flops;
+    }
+    int n = 0;
+    for (int k = 0; k < PK_COUNT; ++k) {
+        if (!acc[k].launches) continue;
+        const char* nm = (k == PK_FAST) ? P->fp.name : kProfNames[k];
+        std::snprintf(acc[k].name, sizeof acc[k].name, "%s", nm);
+        if (n < max_stats) stats[n] = acc[k];
+        ++n;
+    }
+    *n_stats = n;
+    P->recs.clear();
+    P->pool_used = 0;
+    return DGT_OK;
+}
+
+int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W) {
+    Plan* P = (Plan*)plan;
+    if (!P || W <= 0) return 0;
+    const int64_t chunks = (W + P->chunk - 1) / P->chunk;
+    int64_t per = P->fast ? fast_launches_per_chunk(&P->fp) : 2;
+    if (P->info.branch == DGT_BRANCH_FREQ) per += 1 + (((P->flags & DGT_REAL_INPUT) || P->pre) ? 1 : 0);
+    return chunks * per;
+}
+
+}  // extern "C"

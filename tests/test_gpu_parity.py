@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): relative l2 error <= 1e-10 for fp64 (c128) and
+<= 2e-5 for fp32 (c64), over the compared coefficients.  Small lattices are compared
+element by element in full; BASELINE.json's configs run at full size in bench.py's
+launch configuration (full W, default chunking) and are compared on sampled signals /
+columns the oracle computes one by one.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from synthetic import CONFIGS, batch, random_pair, window
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c64": 2e-5, "c128": 1e-10}
+
+
+def rel(x, y):
+    return float(np.linalg.norm(x - y) / np.linalg.norm(y))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+@pytest.fixture(scope="module")
+def nsdgt():
+    import paper_1307_4569_b200 as m
+    return m
+
+
+def run_gpu(nsdgt, torch, f, g, L, a, M, l1, l2, dtype, **kw):
+    plan = nsdgt.Plan(L, a, M, l1, l2, g, dtype=dtype, real_input=np.isrealobj(f), **kw)
+    ft = torch.from_numpy(np.ascontiguousarray(f)).cuda()
+    c = plan.execute(ft)
+    torch.cuda.synchronize()
+    return c.cpu().numpy(), plan
+
+
+def small_cases():
+    out = []
+    for L in (24, 36, 48, 60, 72, 96, 120, 144):
+        for a in range(1, L + 1):
+            if L % a:
+                continue
+            for M in range(2, L + 1):
+                if L % M or L * (L // a) * M > 400000 or (L // a) < 2:
+                    continue
+                for l1, l2 in [(0, 1), (1, 2), (1, 3), (2, 3), (1, 4), (3, 4)]:
+                    if (L // M) % l2 or (L // a) % l2:
+                        continue
+                    out.append((L, a, M, l1, l2))
+    rng = np.random.default_rng(3)
+    idx = rng.choice(len(out), size=min(120, len(out)), replace=False)
+    return [out[i] for i in sorted(idx)]
+
+
+SMALL = small_cases()
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_small_lattice_sweep(torch_cuda, nsdgt, oracle_mod, dtype):
+    """Feasible lattices L <= 144 (both branches, p = 1 and p > 1), full comparison."""
+    worst = 0.0
+    branches = set()
+    for i, (L, a, M, l1, l2) in enumerate(SMALL):
+        f, g = random_pair(L, 100 + i, dtype=dtype)
+        c, plan = run_gpu(nsdgt, torch_cuda, f, g, L, a, M, l1, l2, dtype)
+        branches.add(plan.info["branch"])
+        ref = oracle_mod.dgt(f, g, a, M, l1, l2, variant="literal")
+        e = rel(c, ref)
+        worst = max(worst, e)
+        assert e <= TOL[dtype], (L, a, M, l1, l2, plan.info, e)
+    assert branches == {0, 1, 2}
+
+
+@pytest.mark.parametrize("L,a,M,l1,l2", [(36, 6, 6, 1, 3), (96, 8, 12, 1, 2), (72, 6, 8, 1, 3), (240, 8, 12, 1, 2),
+                                         (160, 10, 8, 1, 4)])
+def test_every_valid_shear_same_c(torch_cuda, nsdgt, oracle_mod, L, a, M, l1, l2):
+    """Every (s0, s1) satisfying Eq. (modcond) gives the same c (reading Z9), incl. the
+    paper's own s1 choice (Eq. s1choice)."""
+    f, g = random_pair(L, 7, dtype="c128")
+    ref = oracle_mod.dgt(f, g, a, M, l1, l2, variant="literal")
+    base = nsdgt.lattice_plan(L, a, M, l1, l2)
+    tried = 0
+    for s1 in range(base["b"]):
+        shear = None
+        for s0 in range(L):
+            try:
+                nsdgt.lattice_plan(L, a, M, l1, l2, shear=(s0, s1))
+                shear = (s0, s1)
+                break
+            except nsdgt.DgtError:
+                continue
+        if shear is None:
+            continue
+        c, plan = run_gpu(nsdgt, torch_cuda, f, g, L, a, M, l1, l2, "c128", shear=shear)
+        assert rel(c, ref) <= 1e-10, (shear, plan.info)
+        tried += 1
+    c, _ = run_gpu(nsdgt, torch_cuda, f, g, L, a, M, l1, l2, "c128", paper_shear=True)
+    assert rel(c, ref) <= 1e-10
+    assert tried >= 1
+
+
+def test_real_input_config1(torch_cuda, nsdgt, oracle_mod):
+    """Config 1 exactly as in BASELINE.json: real fp64 f, pgauss window, frequency shear."""
+    wl = CONFIGS[0]
+    f = batch(wl, 0, wl.W)
+    g = window(wl)
+    c, plan = run_gpu(nsdgt, torch_cuda, f, g, wl.L, wl.a, wl.M, wl.lam1, wl.lam2, wl.dtype)
+    assert plan.info["branch"] == 2 and plan.info["p"] == 2
+    ref = oracle_mod.dgt(f, g, wl.a, wl.M, wl.lam1, wl.lam2, variant="literal")
+    assert rel(c, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_baseline_config_full_size(torch_cuda, nsdgt, oracle_mod, k):
+    """BASELINE configs at full size and full W (bench.py's launch configuration).
+    Whole signals are compared for a few w; every other w is compared on sampled columns."""
+    wl = CONFIGS[k - 1]
+    torch = torch_cuda
+    g = window(wl)
+    f = batch(wl, 0, wl.W)
+    plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
+    c = plan.execute(torch.from_numpy(f).cuda())
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(k)
+    full_ws = [0] if k in (4,) else [0, wl.W - 1]
+    for w in sorted(set(full_ws)):
+        if k == 4:
+            cols = np.sort(rng.choice(wl.N, 96, replace=False))
+            ref = oracle_mod.dgt(f[w], g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols)
+            got = c[w][:, torch.from_numpy(cols).cuda()].cpu().numpy()
+        else:
+            ref = oracle_mod.dgt(f[w], g, wl.a, wl.M, wl.lam1, wl.lam2)
+            got = c[w].cpu().numpy()
+        assert rel(got, ref) <= TOL[wl.dtype], (k, w)
+    # sampled signals x sampled columns
+    ws = np.sort(rng.choice(wl.W, min(wl.W, 6), replace=False))
+    cols = np.sort(rng.choice(wl.N, 8, replace=False))
+    ref = oracle_mod.dgt(f[ws], g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols)
+    got = c[torch.from_numpy(ws).cuda()][:, :, torch.from_numpy(cols).cuda()].cpu().numpy()
+    assert rel(got, ref) <= TOL[wl.dtype]
+
+
+@pytest.mark.parametrize("k", [3, 5])
+def test_delta_window_full_size(torch_cuda, nsdgt, k):
+    """Full-size invariant (no oracle): g = delta_0 => c(m,n) = f(an) e^{-2 pi i (m+w(n)) a n / M}."""
+    wl = CONFIGS[k - 1]
+    torch = torch_cuda
+    g = np.zeros(wl.L, dtype=np.complex64 if wl.dtype == "c64" else np.complex128)
+    g[0] = 1
+    W = 8
+    f = batch(wl, 0, W)
+    plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
+    c = plan.execute(torch.from_numpy(f).cuda()).cpu().numpy()
+    m = np.arange(wl.M)[:, None]
+    n = np.arange(wl.N)[None, :]
+    num = ((m * wl.lam2 + (n * wl.lam1) % wl.lam2) * wl.a * n) % (wl.lam2 * wl.M)
+    ph = np.exp(-2j * np.pi * num / (wl.lam2 * wl.M))
+    for w in range(W):
+        ref = f[w][wl.a * n].astype(np.complex128) * ph
+        assert rel(c[w], ref) <= TOL[wl.dtype]
+
+
+def test_chunking_ragged_and_host_path(torch_cuda, nsdgt):
+    """Ragged chunks (W not a multiple of the chunk), W = 0, and the host end-to-end path
+    give bitwise the same result as one device execute."""
+    torch = torch_cuda
+    L, a, M, l1, l2 = 4096, 32, 64, 1, 2
+    rng = np.random.default_rng(9)
+    W = 7
+    f = (rng.standard_normal((W, L)) + 1j * rng.standard_normal((W, L))).astype(np.complex64)
+    _, g = random_pair(L, 3, dtype="c64")
+    p1 = nsdgt.Plan(L, a, M, l1, l2, g, dtype="c64")
+    p3 = nsdgt.Plan(L, a, M, l1, l2, g, dtype="c64", max_chunk=3)
+    ft = torch.from_numpy(f).cuda()
+    c1 = p1.execute(ft).cpu().numpy()
+    c3 = p3.execute(ft).cpu().numpy()
+    assert np.array_equal(c1, c3)
+    ch = p3.execute_host(f)
+    assert np.array_equal(ch, c1)
+    pinned = torch.from_numpy(f).pin_memory()
+    ch2 = p3.execute_host(pinned)
+    assert np.array_equal(ch2.numpy(), c1)
+    empty = p1.execute(torch.empty((0, L), dtype=torch.complex64, device="cuda"))
+    assert empty.shape == (0, M, L // a)
+
+
+def test_linearity_and_determinism(torch_cuda, nsdgt):
+    torch = torch_cuda
+    wl = CONFIGS[2]
+    g = window(wl)
+    f = batch(wl, 0, 3)
+    plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
+    ft = torch.from_numpy(f).cuda()
+    c = plan.execute(ft)
+    c2 = plan.execute(ft)
+    assert torch.equal(c, c2)
+    s = plan.execute((ft[0:1] + 2 * ft[1:2]).contiguous())
+    assert rel((c[0] + 2 * c[1]).cpu().numpy(), s[0].cpu().numpy()) < 1e-5
+
+
+def test_fast_path_matches_generic(torch_cuda, nsdgt):
+    """Where a specialised kernel exists it agrees with the generic kernels."""
+    torch = torch_cuda
+    for k in (3, 5, 2, 4):
+        wl = CONFIGS[k - 1]
+        g = window(wl)
+        f = batch(wl, 0, 2)
+        pf = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
+        pg = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, force_generic=True)
+        assert pg.info["kernel_path"] == 0
+        ft = torch.from_numpy(f).cuda()
+        a_ = pf.execute(ft).cpu().numpy()
+        b_ = pg.execute(ft).cpu().numpy()
+        assert rel(a_, b_) <= TOL[wl.dtype]
+
+
+def test_errors_on_gpu(torch_cuda, nsdgt):
+    torch = torch_cuda
+    with pytest.raises(nsdgt.DgtError) as ei:
+        nsdgt.Plan(100, 8, 12, 1, 2, np.ones(100), dtype="c64")
+    assert ei.value.status == 4 and ei.value.L_min == 48
+    plan = nsdgt.Plan(48, 4, 6, 1, 2, np.ones(48), dtype="c64")
+    with pytest.raises(TypeError):
+        plan.execute(torch.zeros(48, dtype=torch.complex128, device="cuda"))
