@@ -628,11 +628,10 @@ static int configure(Plan* P, int64_t max_chunk) {
 static int alloc_workspace(Plan* P, int64_t Wc) {
     const dgt_lattice_info& I = P->info;
     if (P->Cws) return DGT_OK;
-    size_t need = (size_t)Wc * I.iM * I.iN * P->esz;
-    if (P->fast) need = std::max(need, fast_workspace_bytes(&P->fp, Wc));
+    size_t need = P->fast ? fast_workspace_bytes(&P->fp, Wc) : (size_t)Wc * I.iM * I.iN * P->esz;
     CUDA_TRY(cudaMalloc(&P->Cws, need));
     P->ws_bytes = need;
-    if (I.branch == DGT_BRANCH_FREQ) {
+    if (I.branch == DGT_BRANCH_FREQ && !P->fast) {
         CUDA_TRY(cudaMalloc(&P->fhat, (size_t)Wc * I.L * P->esz));
         P->ws_bytes += (size_t)Wc * I.L * P->esz;
     }
@@ -854,7 +853,7 @@ int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W) {
     Plan* P = (Plan*)plan;
     if (!P || W <= 0) return 0;
     const int64_t chunks = (W + P->chunk - 1) / P->chunk;
-    int64_t per = P->fast ? fast_launches_per_chunk(&P->fp) : 2;
+    int64_t per = P->fast ? fast_launches_per_chunk(&P->fp) + 1 /* counter memset */ : 2;
     if (P->info.branch == DGT_BRANCH_FREQ) per += 1 + (((P->flags & DGT_REAL_INPUT) || P->pre) ? 1 : 0);
     return chunks * per;
 }

@@ -165,8 +165,11 @@ class Plan:
 
     def close(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            _lib.dgt_destroy(h)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.dgt_destroy(h)
+            except Exception:  # noqa: BLE001  (interpreter shutdown)
+                pass
             self._h = None
 
     def launches(self, W: int) -> int:
