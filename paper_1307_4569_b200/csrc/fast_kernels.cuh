@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -45,11 +46,22 @@ template <int E> struct WarpFftShape {
     static constexpr int SCRATCH = E * SROW;           // complex elements per warp
 };
 
+// W_32^k as compile-time constants (pass-2 twiddles when H = 2: only lanes h = 1 multiply)
+__device__ __forceinline__ float2 w32(int k) {
+    // table of exp(-2 pi i k/32), k < 16 (constant memory broadcast: k is warp-uniform)
+    constexpr float c[16] = {1.0f, 0.98078528040323044913f, 0.92387953251128675613f, 0.83146961230254523708f,
+                             0.70710678118654752440f, 0.55557023301960222474f, 0.38268343236508977173f,
+                             0.19509032201612826785f, 0.0f, -0.19509032201612826785f, -0.38268343236508977173f,
+                             -0.55557023301960222474f, -0.70710678118654752440f, -0.83146961230254523708f,
+                             -0.92387953251128675613f, -0.98078528040323044913f};
+    return make_float2(c[k], c[(k + 8) & 15] * (k < 8 ? 1.0f : -1.0f));  // (cos, -sin)
+}
+
 template <typename T, int E>
 struct WarpFft {
     using S = WarpFftShape<E>;
-    cx<T> tw1[E];  // W_N^{lane*k1}
-    cx<T> tw2[E];  // W_32^{h*k'}, h = lane / E
+    cx<T> tw1[E];                   // W_N^{lane*k1}
+    cx<T> tw2[S::H == 2 ? 1 : E];   // W_32^{h*k'}, h = lane / E (registers only when H > 2)
 
     __device__ __forceinline__ void init(int lane) {
         const int h = lane / E;
@@ -58,8 +70,10 @@ struct WarpFft {
             double s, c;
             sincospi(-2.0 * (double)((lane * k) % S::N) / (double)S::N, &s, &c);
             tw1[k] = mk<T>((T)c, (T)s);
-            sincospi(-2.0 * (double)((h * k) % 32) / 32.0, &s, &c);
-            tw2[k] = mk<T>((T)c, (T)s);
+            if constexpr (S::H != 2) {
+                sincospi(-2.0 * (double)((h * k) % 32) / 32.0, &s, &c);
+                tw2[k] = mk<T>((T)c, (T)s);
+            }
         }
     }
     // output index j-block of this lane (cross-lane DFT-H leaves outputs bit reversed)
@@ -81,8 +95,15 @@ struct WarpFft {
         for (int m = 0; m < E; ++m) v[m] = scr[k1 * S::SROW + h + S::H * m];
         __syncwarp();
         dft_fixed<T, E>(v);
+        if constexpr (S::H == 2) {
+            if (h) {
 #pragma unroll
-        for (int k = 1; k < E; ++k) v[k] = cmul(v[k], tw2[k]);
+                for (int k = 1; k < E; ++k) v[k] = cmul(v[k], w32(k));
+            }
+        } else {
+#pragma unroll
+            for (int k = 1; k < E; ++k) v[k] = cmul(v[k], tw2[k]);
+        }
         if constexpr (S::H >= 4) {
             // DIF radix-2 on lane bit 2E: lanes h<2 keep Z_h + Z_{h+2}; h>=2 get (Z_{h-2} - Z_h) W4^{h-2}
             const bool hi = (h & 2) != 0;
@@ -123,9 +144,11 @@ struct FusedArgs {
     int Kmod;           // K mod D
     const void* E;      // [N] Alg. 1 column phase
     const int* rot;     // [N] Alg. 1 row rotation
-    int* counters;      // [1 + 2W]
+    int* counters;      // [ngroups] group-barrier counters (zeroed per launch)
     int64_t W, L;
-    int c, N, S, lag, nA, nB;
+    int c, N, nA, nB;
+    int GS, ngroups;    // CTAs per group; groups (each group owns one signal at a time)
+    int dbg;            // experiment knobs (0 in production)
 };
 
 struct Job {
@@ -164,26 +187,100 @@ template <typename T, int D, int MM, int Q>
 struct FusedCfg {
     static constexpr int ED = D / 32, EM = MM / 32;
     static constexpr int NWARP = 16, NTHR = 512;
-    static constexpr int SF = D + 1;        // Fh row stride
-    static constexpr int SI = MM + 1;       // In row stride
-    static constexpr int SO = 18;           // Out row stride (16 cols + pad, 16-byte aligned rows)
+    static constexpr int ROWS = D > MM ? D : MM;
+    static constexpr int TILE = ROWS * 16;    // row-major, 16 complex per row, 16-byte chunks XOR-swizzled
     static constexpr int SCR = (WarpFftShape<ED>::SCRATCH > WarpFftShape<EM>::SCRATCH ? WarpFftShape<ED>::SCRATCH
                                                                                        : WarpFftShape<EM>::SCRATCH);
-    // A: Fh[16][SF] + scratch[16][SCR];  B: max(In[16][SI], scratch[16][SCR]) + Out[MM][SO]
-    static constexpr size_t A_ELEMS = (size_t)16 * SF + (size_t)NWARP * SCR;
-    static constexpr size_t B_ELEMS = ((size_t)16 * SI > (size_t)NWARP * SCR ? (size_t)16 * SI : (size_t)NWARP * SCR) +
-                                      (size_t)MM * SO;
-    static constexpr size_t SMEM = sizeof(cx<T>) * (A_ELEMS > B_ELEMS ? A_ELEMS : B_ELEMS);
+    static constexpr int FH = 16 * (D + 1);   // per-warp F^ rows (A jobs)
+    static constexpr int OUT = MM * 16;       // output staging (B jobs), aliases FH
+    static constexpr int U = FH > OUT ? FH : OUT;
+    static constexpr size_t ELEMS = (size_t)TILE + (size_t)NWARP * SCR + (size_t)U;
+    static constexpr size_t SMEM = sizeof(cx<T>) * ELEMS;
 };
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Group barrier over the GS CTAs of one group (all CTAs are co-resident: persistent grid).
+__device__ __forceinline__ void group_barrier(int* cnt, int target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(cnt, 1);
+        while (ld_acquire(cnt) < target) __nanosleep(32);
+    }
+    __syncthreads();
+}
+
+// Static schedule of one CTA: for each signal of its group, its A jobs, a group barrier,
+// its B jobs, a group barrier.  Position k -> (w, isA, job); false past the end.
+struct CtaSchedule {
+    int64_t W;
+    int ngroups, g, q, GS, perA, perB;
+    __device__ __forceinline__ bool at(int64_t k, int64_t* w, int* isA, int* job) const {
+        const int per = perA + perB;
+        const int64_t round = k / per;
+        const int r = (int)(k % per);
+        *w = g + round * ngroups;
+        if (*w >= W) return false;
+        if (r < perA) { *isA = 1; *job = q + r * GS; }
+        else { *isA = 0; *job = q + (r - perA) * GS; }
+        return true;
+    }
+};
+
+// Tile element (row, col) -> position: row-major rows of 16 complex, chunk (2 complex) index
+// XOR-swizzled with (row & 7) so column reads are at most 4-way bank conflicted.
+__device__ __forceinline__ int tile_pos(int row, int col) {
+    return row * 16 + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
+}
+
+// Issue the cp.async copies of one job's tile (16-byte chunks, full 32-byte sectors).
+//  A job (4 residues r0.. x 4 l): row s, col = rho + 4 l  <- f[w][s M + c l + r0 + rho]
+//  B job (16 columns n = 16 t + kappa + 4 n''): row j, col = kappa + 4 n'' <- C[j][kappa][4t + n'']
+template <typename T, int D, int MM, int Q>
+__device__ __forceinline__ void issue_tile(cx<T>* tile, const FusedArgs& A, const cx<T>* ws, int64_t w, int isA,
+                                           int job) {
+    using Cfg = FusedCfg<T, D, MM, Q>;
+    constexpr int NT = Cfg::NTHR;
+    const int tid = threadIdx.x;
+    if (isA) {
+        const cx<T>* fw = (const cx<T>*)A.f + w * A.L + 4 * job;
+#pragma unroll
+        for (int i = 0; i < D * 8 / NT; ++i) {
+            const int e = tid + NT * i;
+            const int s = e >> 3, ch = e & 7, l = ch >> 1, hf = ch & 1;   // col = 2 hf + 4 l (+0/1)
+            cp_async16(tile + s * 16 + ((ch ^ (s & 7)) << 1), fw + (int64_t)s * MM + A.c * l + 2 * hf);
+        }
+    } else {
+        const cx<T>* src = ws + 4 * job;
+#pragma unroll
+        for (int i = 0; i < MM * 8 / NT; ++i) {
+            const int e = tid + NT * i;
+            const int jj = e >> 3, ch = e & 7, kap = ch >> 1, hf = ch & 1;  // cols kap + 4 (2hf), kap + 4 (2hf+1)
+            // chunk holds n'' = 2hf, 2hf+1 of kappa: logical cols (kap + 8 hf) and (kap + 8 hf + 4)
+            cp_async16(tile + jj * 16 + ((ch ^ (jj & 7)) << 1), src + ((int64_t)jj * Q + kap) * D + 2 * hf);
+        }
+    }
+    cp_async_commit();
+}
 
 template <typename T, int D, int MM, int Q>
 __global__ void __launch_bounds__(512, 1) fused_t_kernel(FusedArgs A) {
     using C = cx<T>;
     using Cfg = FusedCfg<T, D, MM, Q>;
-    constexpr int ED = Cfg::ED, EM = Cfg::EM;
+    constexpr int ED = Cfg::ED, EM = Cfg::EM, NT = Cfg::NTHR;
+    static_assert(sizeof(C) == 8, "fused path is complex64");
+    static_assert(Q == 4, "fused path assumes q = 4");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* sm = (C*)smem_raw;
-    __shared__ int s_job;
+    C* tile = sm;
+    C* scr = sm + Cfg::TILE + (threadIdx.x >> 5) * Cfg::SCR;
+    C* uni = sm + Cfg::TILE + Cfg::NWARP * Cfg::SCR;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     WarpFft<T, ED> fftD;
     fftD.init(lane);
@@ -192,68 +289,85 @@ __global__ void __launch_bounds__(512, 1) fused_t_kernel(FusedArgs A) {
     const WarpFft<T, EM>& fM = [&]() -> const WarpFft<T, EM>& {
         if constexpr (EM == ED) return fftD; else return fftM;
     }();
-    const int64_t total = A.W * (int64_t)(A.nA + A.nB);
-    int* queue = A.counters;
-    int* doneA = A.counters + 1;
-    int* doneB = A.counters + 1 + A.W;
-    const C* __restrict__ f = (const C*)A.f;
+    CtaSchedule sch;
+    sch.W = A.W; sch.ngroups = A.ngroups; sch.g = blockIdx.x / A.GS; sch.q = blockIdx.x % A.GS; sch.GS = A.GS;
+    sch.perA = A.nA > sch.q ? (A.nA - sch.q + A.GS - 1) / A.GS : 0;
+    sch.perB = A.nB > sch.q ? (A.nB - sch.q + A.GS - 1) / A.GS : 0;
+    if (sch.g >= A.ngroups) return;
+    int* bar = A.counters + sch.g;
+    int epoch = 0;
     const C* __restrict__ G = (const C*)A.G;
     const int c = A.c;
-    const int64_t slot_elems = (int64_t)MM * Q * D;
+    C* ws = (C*)A.ws + (int64_t)sch.g * MM * Q * D;   // this group's intermediate C[j][kappa][n']
 
-    for (;;) {
-        if (tid == 0) s_job = atomicAdd(queue, 1);
-        __syncthreads();
-        const int64_t p = s_job;
-        if (p >= total) break;
-        const Job jb = decode_job(p, A.W, A.lag, A.nA, A.nB);
-        if (tid == 0) {
-            if (jb.isA) {
-                if (jb.w >= A.S)
-                    while (ld_acquire(&doneB[jb.w - A.S]) < A.nB) __nanosleep(100);
-            } else {
-                while (ld_acquire(&doneA[jb.w]) < A.nA) __nanosleep(100);
-            }
+    // a CTA with no jobs still takes part in its group's barriers
+    if (sch.perA + sch.perB == 0) {
+        for (int64_t w = sch.g; w < A.W; w += A.ngroups) {
+            group_barrier(bar, (++epoch) * A.GS);
+            group_barrier(bar, (++epoch) * A.GS);
         }
-        __syncthreads();
-        C* ws = (C*)A.ws + (int64_t)(jb.w % A.S) * slot_elems;
-        if (jb.isA) {
-            // ---------------- A job: 16 Zak columns (4 residues x Q=4 l) ----------------
-            C* Fh = sm;
-            C* scr = sm + 16 * Cfg::SF + warp * Cfg::SCR;
+        return;
+    }
+    // the schedule visits A (perA) then B (perB) jobs per signal; phases with zero jobs still
+    // need their barrier, handled by the transition logic below
+    int64_t w;
+    int isA, job;
+    int64_t k = 0;
+    bool have = sch.at(0, &w, &isA, &job);
+    bool issued = false;
+    if (have && isA) { issue_tile<T, D, MM, Q>(tile, A, ws, w, 1, job); issued = true; }
+    int64_t cur_w = sch.g;   // signal whose phases we are in
+    int phase = 0;           // 0 = A phase of cur_w, 1 = B phase of cur_w
+    while (have) {
+        // advance phases (with their barriers) until (w, isA) is reached
+        while (cur_w != w || phase != (isA ? 0 : 1)) {
+            group_barrier(bar, (++epoch) * A.GS);
+            if (phase == 0) phase = 1; else { phase = 0; cur_w += A.ngroups; }
+        }
+        if (!issued) issue_tile<T, D, MM, Q>(tile, A, ws, w, isA, job);
+        cp_async_wait_all();
+        __syncthreads();  // tile k visible; previous job's Out fully stored
+        int64_t w2; int isA2, job2;
+        const bool more = sch.at(k + 1, &w2, &isA2, &job2);
+        // the next tile may be prefetched now unless it is a B tile behind a group barrier
+        const bool can_pf = more && (isA2 || (!isA && w2 == w));
+        if (isA) {
+            // -------- A job: 16 Zak columns = 4 residues (rho) x 4 l; warp = rho + 4 l --------
             const int rho = warp & 3, l = warp >> 2;
-            const int r = 4 * jb.idx + rho;
+            const int r = 4 * job + rho;
             const int j = r + c * l;
-            const C* fw = f + (int64_t)jb.w * A.L;
             C v[ED];
 #pragma unroll
-            for (int k = 0; k < ED; ++k) v[k] = __ldg(fw + (int64_t)(lane + 32 * k) * MM + j);
+            for (int kk = 0; kk < ED; ++kk) v[kk] = tile[tile_pos(lane + 32 * kk, warp)];
+            __syncthreads();  // tile consumed
+            issued = false;
+            if (can_pf) { issue_tile<T, D, MM, Q>(tile, A, ws, w2, isA2, job2); issued = true; }
             if (A.Rs) {
                 const C* Rs = (const C*)A.Rs;
 #pragma unroll
-                for (int k = 0; k < ED; ++k) v[k] = cmul(v[k], __ldg(Rs + lane + 32 * k));
+                for (int kk = 0; kk < ED; ++kk) v[kk] = cmul(v[kk], __ldg(Rs + lane + 32 * kk));
             }
             fftD.run(v, scr, lane);
             if (A.Cj) {
                 const C cj = __ldg((const C*)A.Cj + j);
 #pragma unroll
-                for (int k = 0; k < ED; ++k) v[k] = cmul(v[k], cj);
+                for (int kk = 0; kk < ED; ++kk) v[kk] = cmul(v[kk], cj);
             }
+            C* Frow = uni + warp * (D + 1);
             {
                 const int k1 = lane % ED, jo = WarpFft<T, ED>::out_jo(lane);
 #pragma unroll
-                for (int k = 0; k < ED; ++k) Fh[warp * Cfg::SF + k1 + ED * k + ED * ED * jo] = v[k];
+                for (int kk = 0; kk < ED; ++kk) Frow[k1 + ED * kk + ED * ED * jo] = v[kk];
             }
-            __syncthreads();
+            __syncwarp();
             const int shift = (int)(((int64_t)A.Kmod * j) % D);
-            const C* Frow = Fh + warp * Cfg::SF;
 #pragma unroll 1
             for (int u = 0; u < Q; ++u) {
                 const C* Gr = G + ((int64_t)r * Q + u) * D;
 #pragma unroll
-                for (int k = 0; k < ED; ++k) {
-                    const int nu = lane + 32 * k;
-                    v[k] = cmul(Frow[(nu - shift) & (D - 1)], __ldg(Gr + nu));
+                for (int kk = 0; kk < ED; ++kk) {
+                    const int nu = lane + 32 * kk;
+                    v[kk] = cmul(Frow[(nu - shift) & (D - 1)], __ldg(Gr + nu));
                 }
                 fftD.run(v, scr, lane);
                 // T_r(l,u;tau) -> C[j][kappa][n'], kappa = (l-u) mod Q, n' = (-tau - [l<u]) mod D
@@ -261,58 +375,57 @@ __global__ void __launch_bounds__(512, 1) fused_t_kernel(FusedArgs A) {
                 const int off = (l < u) ? 1 : 0;
                 C* dst = ws + ((int64_t)j * Q + kappa) * D;
                 const int k1 = lane % ED, jo = WarpFft<T, ED>::out_jo(lane);
+                const int base = -(k1 + ED * ED * jo) - off;
 #pragma unroll
-                for (int k = 0; k < ED; ++k) {
-                    const int tau = k1 + ED * k + ED * ED * jo;
-                    __stcg(dst + ((-tau - off) & (D - 1)), v[k]);
-                }
+                for (int kk = 0; kk < ED; ++kk) __stcg(dst + ((base - ED * kk) & (D - 1)), v[kk]);
             }
         } else {
-            // ---------------- B job: 16 consecutive columns n ----------------
-            C* In = sm;
-            C* scr = sm + warp * Cfg::SCR;  // aliases In after the columns are in registers
-            C* Out = sm + (16 * Cfg::SI > 16 * Cfg::SCR ? 16 * Cfg::SI : 16 * Cfg::SCR);
-            const int t = jb.idx;
-            const int n0p = 4 * t;  // n' block
-            // load C[j][kappa][n0p..n0p+4) for all j, kappa -> In[col][j], col = kappa + 4 n''
-            for (int e = tid; e < MM * Q * 2; e += Cfg::NTHR) {
-                const int half = e & 1, kap = (e >> 1) % Q, jj = (e >> 1) / Q;
-                const C* src = ws + ((int64_t)jj * Q + kap) * D + n0p + 2 * half;
-                const C a0 = ldcg<T>(src), a1 = ldcg<T>(src + 1);
-                In[(kap + Q * (2 * half)) * Cfg::SI + jj] = a0;
-                In[(kap + Q * (2 * half + 1)) * Cfg::SI + jj] = a1;
-            }
-            __syncthreads();
+            // -------- B job: 16 consecutive columns n = 16 t + col, col = kappa + 4 n'' --------
+            const int t = job;
+            // tile chunk layout: chunk (kap, hf) holds n'' = 2hf, 2hf+1 -> logical col index
+            // used by tile_pos is cl = 2*(2 kap + hf) + (n'' & 1)
+            const int kap = warp & 3, nn = warp >> 2;
+            const int cl = 2 * (2 * kap + (nn >> 1)) + (nn & 1);
             C v[EM];
 #pragma unroll
-            for (int k = 0; k < EM; ++k) v[k] = In[warp * Cfg::SI + lane + 32 * k];
-            __syncthreads();
+            for (int kk = 0; kk < EM; ++kk) v[kk] = tile[tile_pos(lane + 32 * kk, cl)];
+            __syncthreads();  // tile consumed
+            issued = false;
+            if (can_pf) { issue_tile<T, D, MM, Q>(tile, A, ws, w2, isA2, job2); issued = true; }
             fM.run(v, scr, lane);
-            const int n = 16 * t + warp;
+            C* Out = uni;
+            const int n = 16 * t + warp;   // warp = kappa + 4 n''
             const C e = __ldg((const C*)A.E + n);
             const int rt = __ldg(A.rot + n);
             const int k1 = lane % EM, jo = WarpFft<T, EM>::out_jo(lane);
 #pragma unroll
-            for (int k = 0; k < EM; ++k) {
-                const int m = k1 + EM * k + EM * EM * jo;
+            for (int kk = 0; kk < EM; ++kk) {
+                const int m = k1 + EM * kk + EM * EM * jo;
                 const int mo = (m - rt) & (MM - 1);
-                Out[mo * Cfg::SO + warp] = cmul(e, v[k]);
+                Out[mo * 16 + (warp ^ (mo & 15))] = cmul(e, v[kk]);
             }
             __syncthreads();
-            C* cw = (C*)A.out + (int64_t)jb.w * MM * A.N + 16 * t;
-            constexpr int VPR = 16 * (int)sizeof(C) / 16;  // 16-byte vectors per output row
-            for (int e2 = tid; e2 < MM * VPR; e2 += Cfg::NTHR) {
-                const int mo = e2 / VPR, part = e2 % VPR;
-                const float4 val = *(const float4*)((const char*)(Out + mo * Cfg::SO) + 16 * part);
-                __stcs((float4*)((char*)(cw + (int64_t)mo * A.N) + 16 * part), val);
+            C* cw = (C*)A.out + w * MM * A.N + 16 * t;
+            constexpr int PER2 = MM * 8 / NT;
+#pragma unroll
+            for (int i = 0; i < PER2; ++i) {
+                const int e2 = tid + NT * i;
+                const int mo = e2 >> 3, pp = e2 & 7, sw = mo & 15;
+                float4 val = *(const float4*)(Out + mo * 16 + 2 * (pp ^ (sw >> 1)));
+                if (sw & 1) val = make_float4(val.z, val.w, val.x, val.y);
+                __stcs((float4*)(cw + (int64_t)mo * A.N + 2 * pp), val);
             }
         }
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            atomicAdd(jb.isA ? &doneA[jb.w] : &doneB[jb.w], 1);
-        }
+        ++k;
+        have = more;
+        if (have) { w = w2; isA = isA2; job = job2; }
     }
+    // finish this CTA's remaining barriers (its last signal's phases)
+    while (cur_w < A.W) {
+        group_barrier(bar, (++epoch) * A.GS);
+        if (phase == 0) phase = 1; else { phase = 0; cur_w += A.ngroups; }
+    }
+    cp_async_wait_all();
 }
 
 // ------------------------------------------------------------------------------------
@@ -323,7 +436,7 @@ struct FastPlan {
     const char* name = "none";
     int D = 0, MM = 0, Q = 0, c = 0, N = 0;
     int64_t L = 0;
-    int S = 4, lag = 2, nA = 0, nB = 0;
+    int nA = 0, nB = 0, GS = 16, ngroups = 1;
     int grid = 0;
     size_t smem = 0;
     size_t esz = 8;
@@ -334,13 +447,28 @@ struct FastPlan {
     const void* E = nullptr;
     const int* rot = nullptr;
     int* counters = nullptr;
-    int64_t counters_W = 0;
-    void (*launch)(const FusedArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
+    void (*launch)(const FusedArgs&, int grid, size_t smem, cudaStream_t, const cudaAccessPolicyWindow*) = nullptr;
+    bool persist = false;   // L2 persisting window over the intermediate workspace
 };
 
 template <typename T, int D, int MM, int Q>
-void launch_fused(const FusedArgs& a, int grid, size_t smem, cudaStream_t st) {
-    fused_t_kernel<T, D, MM, Q><<<grid, 512, smem, st>>>(a);
+void launch_fused(const FusedArgs& a, int grid, size_t smem, cudaStream_t st, const cudaAccessPolicyWindow* apw) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(FusedCfg<T, D, MM, Q>::NTHR);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    int na = 0;
+    if (apw) {
+        // keep the intermediate ring L2 resident while c streams through
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow = *apw;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, fused_t_kernel<T, D, MM, Q>, a);
 }
 
 template <typename T>
@@ -399,8 +527,19 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, void* G, void* /*chirp*/
     }
     if (rc) return DGT_OK;  // fall back to the generic kernels (still CUDA)
     fp->D = (int)D; fp->MM = (int)MM; fp->Q = (int)I.q; fp->c = (int)I.c; fp->N = (int)I.N; fp->L = I.L;
-    fp->nA = (int)(I.c / 4);
-    fp->nB = (int)(D / 4);
+    fp->nA = (int)(I.c / 4);   // 16 columns (4 residues x 4 l) per A job
+    fp->nB = (int)(D / 4);     // 16 consecutive columns n per B job
+    // groups of GS CTAs each own one signal at a time; the intermediates of the signals in
+    // flight (ngroups x per-signal bytes) must stay L2 resident
+    {
+        const size_t per_sig = (size_t)MM * I.q * D * sizeof(cx<T>);
+        const int max_inflight = (int)std::max<size_t>(1, (size_t)(72u << 20) / per_sig);
+        int gs = 4;
+        while (gs < 64 && (fp->grid / gs) > max_inflight) gs *= 2;
+        if (const char* e = std::getenv("NSDGT_GS")) gs = std::max(1, std::atoi(e));
+        fp->GS = std::min(gs, fp->grid);
+        fp->ngroups = std::max(1, fp->grid / fp->GS);
+    }
     fp->esz = sizeof(cx<T>);
     fp->G = G; fp->E = E; fp->rot = rot;
     // chirp factorisation: K = sigma (L+1) mod 2L
@@ -415,6 +554,7 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, void* G, void* /*chirp*/
         const int64_t n = std::max<int64_t>(MM, D);
         k_chirp_factors<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>((cx<T>*)fp->Cj, (cx<T>*)fp->Rs, K, L, MM, D);
     }
+    fp->persist = std::getenv("NSDGT_PERSIST") != nullptr;  // experiment only
     fp->kind = 1;
     fp->name = "fused_t_p1";
     return DGT_OK;
@@ -429,7 +569,7 @@ inline void free_fast(FastPlan* fp) {
 }
 
 inline size_t fast_workspace_bytes(const FastPlan* fp, int64_t /*Wc*/) {
-    return (size_t)fp->S * fp->MM * fp->Q * fp->D * fp->esz;
+    return (size_t)fp->ngroups * fp->MM * fp->Q * fp->D * fp->esz;
 }
 
 // the fused kernel consumes the whole batch in one launch
@@ -439,21 +579,23 @@ inline int64_t fast_launches_per_chunk(const FastPlan*) { return 1; }
 template <typename T>
 int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int64_t W, cudaStream_t st) {
     if (real_in) return DGT_EUNSUPPORTED;
-    if (fp->counters_W < W) {
-        if (fp->counters) cudaFree(fp->counters);
-        fp->counters = nullptr;
-        fp->counters_W = 0;
-        if (cudaMalloc(&fp->counters, sizeof(int) * (1 + 2 * W)) != cudaSuccess) return DGT_ENOMEM;
-        fp->counters_W = W;
+    if (!fp->counters) {
+        if (cudaMalloc(&fp->counters, sizeof(int) * fp->ngroups) != cudaSuccess) return DGT_ENOMEM;
     }
-    if (cudaMemsetAsync(fp->counters, 0, sizeof(int) * (1 + 2 * W), st) != cudaSuccess) return DGT_ECUDA;
+    if (cudaMemsetAsync(fp->counters, 0, sizeof(int) * fp->ngroups, st) != cudaSuccess) return DGT_ECUDA;
     FusedArgs a{};
     a.f = f; a.ws = ws; a.out = c; a.G = fp->G; a.Cj = fp->Cj; a.Rs = fp->Rs; a.Kmod = fp->Kmod;
     a.E = fp->E; a.rot = fp->rot; a.counters = fp->counters;
-    a.W = W; a.L = fp->L; a.c = fp->c; a.N = fp->N; a.S = fp->S; a.lag = fp->lag; a.nA = fp->nA; a.nB = fp->nB;
-    const int64_t total = W * (int64_t)(fp->nA + fp->nB);
-    const int grid = (int)std::min<int64_t>(fp->grid, total);
-    fp->launch(a, grid, fp->smem, st);
+    a.dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;
+    a.W = W; a.L = fp->L; a.c = fp->c; a.N = fp->N; a.nA = fp->nA; a.nB = fp->nB;
+    a.GS = fp->GS; a.ngroups = fp->ngroups;
+    cudaAccessPolicyWindow apw{};
+    apw.base_ptr = ws;
+    apw.num_bytes = fast_workspace_bytes(fp, W);
+    apw.hitRatio = 1.0f;
+    apw.hitProp = cudaAccessPropertyPersisting;
+    apw.missProp = cudaAccessPropertyStreaming;
+    fp->launch(a, fp->GS * fp->ngroups, fp->smem, st, fp->persist ? &apw : nullptr);
     return DGT_OK;
 }
 
