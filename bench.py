@@ -30,53 +30,28 @@ UNIT = "coefficients/s"
 
 
 def dist_setup(n_gpus):
-    import torch
-    import torch.distributed as dist
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend=backend)
-    if torch.cuda.is_available():
-        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
-    return ws, rank, local
+    from paper_1307_4569_b200 import dist as pd
+    return pd.init()
 
 
 def shard(W, ws, rank):
-    """Contiguous partition of W signals over ws ranks: rank gets [w0, w1)."""
-    w0 = (W * rank) // ws
-    w1 = (W * (rank + 1)) // ws
-    return w0, w1
+    from paper_1307_4569_b200 import dist as pd
+    return pd.shard(W, ws, rank)
 
 
 def barrier(ws):
-    if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    from paper_1307_4569_b200 import dist as pd
+    pd.barrier()
 
 
 def allreduce_max(x, ws):
-    if ws == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_1307_4569_b200 import dist as pd
+    return pd.allreduce(x, "max")
 
 
 def allreduce_sum(x, ws):
-    if ws == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    from paper_1307_4569_b200 import dist as pd
+    return pd.allreduce(x, "sum")
 
 
 class ClockSampler:
