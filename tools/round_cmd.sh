@@ -1,0 +1,12 @@
+# full round check: gpu tests, smoke, bench (cfg5 default), ncu launch list + full capture
+tag=$1
+python -m pytest tests -m gpu -q > gpurun_out/gpu_tests_$tag.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests_$tag.log
+python __graft_entry__.py --smoke > gpurun_out/smoke_$tag.log 2>&1
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv -lms 200 > gpurun_out/clocks_$tag.csv &
+SMI=$!
+python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
+kill $SMI
+python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_$tag.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu1_$tag.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:fused -s 3 -c 1 -o gpurun_out/prof_$tag python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu2_$tag.log 2>&1
+echo done
