@@ -22,6 +22,7 @@
 // so DFT_s[P f](nu, j) = C(j) DFT_s[R f](nu - K j mod d, j): a column phase and a cyclic
 // index shift, no per-sample sincos.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -149,6 +150,8 @@ struct FusedArgs {
     int c, N, nA, nB;
     int GS, ngroups;    // CTAs per group; groups (each group owns one signal at a time)
     int dbg;            // experiment knobs (0 in production)
+    int tma;            // 1: c leaves through TMA bulk-tensor stores (NCOL = 16 only)
+    int discard;        // 1: discard dead intermediate lines from L2 before rewriting them
 };
 
 struct Job {
@@ -183,19 +186,21 @@ template <typename T> __device__ __forceinline__ cx<T> ldcg(const cx<T>* p);
 template <> __device__ __forceinline__ float2 ldcg<float>(const float2* p) { return __ldcg(p); }
 template <> __device__ __forceinline__ double2 ldcg<double>(const double2* p) { return __ldcg(p); }
 
-template <typename T, int D, int MM, int Q>
+template <typename T, int D, int MM, int Q, int NCOL>
 struct FusedCfg {
     static constexpr int ED = D / 32, EM = MM / 32;
-    static constexpr int NWARP = 16, NTHR = 512;
+    static constexpr int NWARP = NCOL, NTHR = 32 * NCOL;   // one warp per column
     static constexpr int ROWS = D > MM ? D : MM;
-    static constexpr int TILE = ROWS * 16;    // row-major, 16 complex per row, 16-byte chunks XOR-swizzled
+    static constexpr int TILE = ROWS * NCOL;  // row-major, NCOL complex per row, 16-byte chunks XOR-swizzled
     static constexpr int SCR = (WarpFftShape<ED>::SCRATCH > WarpFftShape<EM>::SCRATCH ? WarpFftShape<ED>::SCRATCH
                                                                                        : WarpFftShape<EM>::SCRATCH);
-    static constexpr int FH = 16 * (D + 1);   // per-warp F^ rows (A jobs)
-    static constexpr int OUT = MM * 16;       // output staging (B jobs), aliases FH
+    static constexpr int FH = NCOL * (D + 1);   // per-warp F^ rows (A jobs)
+    static constexpr int OUT = MM * NCOL;       // output staging (B jobs), aliases FH
     static constexpr int U = FH > OUT ? FH : OUT;
     static constexpr size_t ELEMS = (size_t)TILE + (size_t)NWARP * SCR + (size_t)U;
     static constexpr size_t SMEM = sizeof(cx<T>) * ELEMS;
+    static constexpr int LPJ = NCOL / 4;        // values of l per A job (4 residues each)
+    static constexpr int NPK = NCOL / 4;        // n' values per kappa per B job
 };
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
@@ -204,6 +209,17 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// TMA (bulk tensor) store of one 2-D box from shared memory; asynchronous (bulk group)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem, int x, int y) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(map), "r"(sa),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // Group barrier over the GS CTAs of one group (all CTAs are co-resident: persistent grid).
 __device__ __forceinline__ void group_barrier(int* cnt, int target) {
@@ -233,54 +249,65 @@ struct CtaSchedule {
     }
 };
 
-// Tile element (row, col) -> position: row-major rows of 16 complex, chunk (2 complex) index
-// XOR-swizzled with (row & 7) so column reads are at most 4-way bank conflicted.
+// Tile element (row, col): row-major rows of NCOL complex; the 16-byte chunk index is
+// XOR-swizzled with the row so that column reads are at most 4-way bank conflicted.
+template <int NCOL>
 __device__ __forceinline__ int tile_pos(int row, int col) {
-    return row * 16 + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
+    return row * NCOL + ((((col >> 1) ^ (row & (NCOL / 2 - 1))) << 1) | (col & 1));
 }
 
-// Issue the cp.async copies of one job's tile (16-byte chunks, full 32-byte sectors).
-//  A job (4 residues r0.. x 4 l): row s, col = rho + 4 l  <- f[w][s M + c l + r0 + rho]
-//  B job (16 columns n = 16 t + kappa + 4 n''): row j, col = kappa + 4 n'' <- C[j][kappa][4t + n'']
-template <typename T, int D, int MM, int Q>
+// Issue the cp.async copies of one job's tile (16-byte chunks, whole 32-byte sectors).
+//  A job (4 residues r0.. x LPJ values of l from l0): row s, col = rho + 4 (l - l0)
+//        <- f[w][s M + c l + r0 + rho];  chunk ch = 2 (l - l0) + hf holds rho = 2hf, 2hf+1
+//  B job (NCOL columns n = NCOL t + kappa + 4 n''): row j, col = 2 chunk + (n'' & 1)
+//        <- C[j][kappa][NPK t + n''];  chunk ch = kappa (NPK/2) + (n'' >> 1)
+template <typename T, int D, int MM, int Q, int NCOL>
 __device__ __forceinline__ void issue_tile(cx<T>* tile, const FusedArgs& A, const cx<T>* ws, int64_t w, int isA,
                                            int job) {
-    using Cfg = FusedCfg<T, D, MM, Q>;
-    constexpr int NT = Cfg::NTHR;
+    using Cfg = FusedCfg<T, D, MM, Q, NCOL>;
+    constexpr int NT = Cfg::NTHR, CPR = NCOL / 2;   // chunks per row
     const int tid = threadIdx.x;
     if (isA) {
-        const cx<T>* fw = (const cx<T>*)A.f + w * A.L + 4 * job;
+        if (A.dbg & 16) { cp_async_commit(); return; }
+        constexpr int JPR = 16 / NCOL;               // A jobs per residue group
+        const int r0 = 4 * (job / JPR), l0 = (job % JPR) * Cfg::LPJ;
+        const cx<T>* fw = (const cx<T>*)A.f + w * A.L + r0;
 #pragma unroll
-        for (int i = 0; i < D * 8 / NT; ++i) {
+        for (int i = 0; i < D * CPR / NT; ++i) {
             const int e = tid + NT * i;
-            const int s = e >> 3, ch = e & 7, l = ch >> 1, hf = ch & 1;   // col = 2 hf + 4 l (+0/1)
-            cp_async16(tile + s * 16 + ((ch ^ (s & 7)) << 1), fw + (int64_t)s * MM + A.c * l + 2 * hf);
+            const int s = e / CPR, ch = e % CPR, ll = ch >> 1, hf = ch & 1;
+            cp_async16(tile + s * NCOL + ((ch ^ (s & (CPR - 1))) << 1),
+                       fw + (int64_t)s * MM + A.c * (l0 + ll) + 2 * hf);
         }
     } else {
-        const cx<T>* src = ws + 4 * job;
+        if (A.dbg & 32) { cp_async_commit(); return; }
+        constexpr int HPK = Cfg::NPK / 2;            // chunks per kappa
+        const cx<T>* src = ws + Cfg::NPK * job;
 #pragma unroll
-        for (int i = 0; i < MM * 8 / NT; ++i) {
+        for (int i = 0; i < MM * CPR / NT; ++i) {
             const int e = tid + NT * i;
-            const int jj = e >> 3, ch = e & 7, kap = ch >> 1, hf = ch & 1;  // cols kap + 4 (2hf), kap + 4 (2hf+1)
-            // chunk holds n'' = 2hf, 2hf+1 of kappa: logical cols (kap + 8 hf) and (kap + 8 hf + 4)
-            cp_async16(tile + jj * 16 + ((ch ^ (jj & 7)) << 1), src + ((int64_t)jj * Q + kap) * D + 2 * hf);
+            const int jj = e / CPR, ch = e % CPR, kap = ch / HPK, hf = ch % HPK;
+            cp_async16(tile + jj * NCOL + ((ch ^ (jj & (CPR - 1))) << 1),
+                       src + ((int64_t)jj * Q + kap) * D + 2 * hf);
         }
     }
     cp_async_commit();
 }
 
-template <typename T, int D, int MM, int Q>
-__global__ void __launch_bounds__(512, 1) fused_t_kernel(FusedArgs A) {
+template <typename T, int D, int MM, int Q, int NCOL>
+__global__ void __launch_bounds__(32 * NCOL, (D <= 256 ? 2 : 1) * (NCOL == 8 ? 2 : 1))
+    fused_t_kernel(FusedArgs A, const __grid_constant__ CUtensorMap cmap) {
     using C = cx<T>;
-    using Cfg = FusedCfg<T, D, MM, Q>;
+    using Cfg = FusedCfg<T, D, MM, Q, NCOL>;
     constexpr int ED = Cfg::ED, EM = Cfg::EM, NT = Cfg::NTHR;
     static_assert(sizeof(C) == 8, "fused path is complex64");
     static_assert(Q == 4, "fused path assumes q = 4");
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    static_assert(NCOL == 8 || NCOL == 16, "8 or 16 columns per job");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     C* sm = (C*)smem_raw;
     C* tile = sm;
     C* scr = sm + Cfg::TILE + (threadIdx.x >> 5) * Cfg::SCR;
-    C* uni = sm + Cfg::TILE + Cfg::NWARP * Cfg::SCR;
+    C* uni = sm + Cfg::TILE + Cfg::NWARP * Cfg::SCR;   // 1024-byte aligned (TMA 128B swizzle)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     WarpFft<T, ED> fftD;
     fftD.init(lane);
@@ -300,31 +327,37 @@ __global__ void __launch_bounds__(512, 1) fused_t_kernel(FusedArgs A) {
     const int c = A.c;
     C* ws = (C*)A.ws + (int64_t)sch.g * MM * Q * D;   // this group's intermediate C[j][kappa][n']
 
-    // a CTA with no jobs still takes part in its group's barriers
-    if (sch.perA + sch.perB == 0) {
+    if (sch.perA + sch.perB == 0) {   // no jobs: still take part in the group's barriers
         for (int64_t w = sch.g; w < A.W; w += A.ngroups) {
             group_barrier(bar, (++epoch) * A.GS);
             group_barrier(bar, (++epoch) * A.GS);
         }
         return;
     }
-    // the schedule visits A (perA) then B (perB) jobs per signal; phases with zero jobs still
-    // need their barrier, handled by the transition logic below
+    if ((A.dbg >> 8) && (sch.g & 1)) {   // experiment: delay odd groups by dbg>>8 microseconds
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > (unsigned long long)(A.dbg >> 8) * 1000ull) break;
+            __nanosleep(1000);
+        }
+    }
     int64_t w;
     int isA, job;
     int64_t k = 0;
     bool have = sch.at(0, &w, &isA, &job);
     bool issued = false;
-    if (have && isA) { issue_tile<T, D, MM, Q>(tile, A, ws, w, 1, job); issued = true; }
+    if (have && isA) { issue_tile<T, D, MM, Q, NCOL>(tile, A, ws, w, 1, job); issued = true; }
     int64_t cur_w = sch.g;   // signal whose phases we are in
     int phase = 0;           // 0 = A phase of cur_w, 1 = B phase of cur_w
     while (have) {
-        // advance phases (with their barriers) until (w, isA) is reached
-        while (cur_w != w || phase != (isA ? 0 : 1)) {
+        while (cur_w != w || phase != (isA ? 0 : 1)) {   // pass the group barriers up to this job
             group_barrier(bar, (++epoch) * A.GS);
             if (phase == 0) phase = 1; else { phase = 0; cur_w += A.ngroups; }
         }
-        if (!issued) issue_tile<T, D, MM, Q>(tile, A, ws, w, isA, job);
+        if (!issued) issue_tile<T, D, MM, Q, NCOL>(tile, A, ws, w, isA, job);
         cp_async_wait_all();
         __syncthreads();  // tile k visible; previous job's Out fully stored
         int64_t w2; int isA2, job2;
@@ -332,28 +365,41 @@ __global__ void __launch_bounds__(512, 1) fused_t_kernel(FusedArgs A) {
         // the next tile may be prefetched now unless it is a B tile behind a group barrier
         const bool can_pf = more && (isA2 || (!isA && w2 == w));
         if (isA) {
-            // -------- A job: 16 Zak columns = 4 residues (rho) x 4 l; warp = rho + 4 l --------
-            const int rho = warp & 3, l = warp >> 2;
-            const int r = 4 * job + rho;
+            // -------- A job: NCOL Zak columns = 4 residues (rho) x LPJ values of l --------
+            constexpr int JPR = 16 / NCOL;
+            const int rho = warp & 3;
+            const int l = (job % JPR) * Cfg::LPJ + (warp >> 2);
+            const int r = 4 * (job / JPR) + rho;
             const int j = r + c * l;
             C v[ED];
 #pragma unroll
-            for (int kk = 0; kk < ED; ++kk) v[kk] = tile[tile_pos(lane + 32 * kk, warp)];
+            for (int kk = 0; kk < ED; ++kk) v[kk] = tile[tile_pos<NCOL>(lane + 32 * kk, warp)];
+            if (A.discard) {
+                // The previous signal's intermediate rows this job is about to overwrite are dead
+                // (its B phase ended at the last group barrier): drop them from L2 without
+                // writing them back to HBM.  Only this CTA writes these rows.
+                C* row = ws + (int64_t)j * Q * D;   // this warp's column j: Q*D complex
+                constexpr int LINES = Q * D * (int)sizeof(C) / 128;
+                for (int i = lane; i < LINES; i += 32)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"((const char*)row + 128 * i) : "memory");
+            }
             __syncthreads();  // tile consumed
             issued = false;
-            if (can_pf) { issue_tile<T, D, MM, Q>(tile, A, ws, w2, isA2, job2); issued = true; }
+            if (can_pf) { issue_tile<T, D, MM, Q, NCOL>(tile, A, ws, w2, isA2, job2); issued = true; }
             if (A.Rs) {
                 const C* Rs = (const C*)A.Rs;
 #pragma unroll
                 for (int kk = 0; kk < ED; ++kk) v[kk] = cmul(v[kk], __ldg(Rs + lane + 32 * kk));
             }
-            fftD.run(v, scr, lane);
+            if (!(A.dbg & 1)) fftD.run(v, scr, lane);
             if (A.Cj) {
                 const C cj = __ldg((const C*)A.Cj + j);
 #pragma unroll
                 for (int kk = 0; kk < ED; ++kk) v[kk] = cmul(v[kk], cj);
             }
             C* Frow = uni + warp * (D + 1);
+            if (tid == 0) bulk_wait_read0();   // the previous output box has left uni
+            __syncthreads();
             {
                 const int k1 = lane % ED, jo = WarpFft<T, ED>::out_jo(lane);
 #pragma unroll
@@ -367,9 +413,9 @@ __global__ void __launch_bounds__(512, 1) fused_t_kernel(FusedArgs A) {
 #pragma unroll
                 for (int kk = 0; kk < ED; ++kk) {
                     const int nu = lane + 32 * kk;
-                    v[kk] = cmul(Frow[(nu - shift) & (D - 1)], __ldg(Gr + nu));
+                    v[kk] = (A.dbg & 64) ? Frow[(nu - shift) & (D - 1)] : cmul(Frow[(nu - shift) & (D - 1)], __ldg(Gr + nu));
                 }
-                fftD.run(v, scr, lane);
+                if (!(A.dbg & 1)) fftD.run(v, scr, lane);
                 // T_r(l,u;tau) -> C[j][kappa][n'], kappa = (l-u) mod Q, n' = (-tau - [l<u]) mod D
                 const int kappa = (l - u + Q) % Q;
                 const int off = (l < u) ? 1 : 0;
@@ -377,66 +423,92 @@ __global__ void __launch_bounds__(512, 1) fused_t_kernel(FusedArgs A) {
                 const int k1 = lane % ED, jo = WarpFft<T, ED>::out_jo(lane);
                 const int base = -(k1 + ED * ED * jo) - off;
 #pragma unroll
-                for (int kk = 0; kk < ED; ++kk) __stcg(dst + ((base - ED * kk) & (D - 1)), v[kk]);
+                if (!(A.dbg & 4))
+                    for (int kk = 0; kk < ED; ++kk) __stcg(dst + ((base - ED * kk) & (D - 1)), v[kk]);
             }
         } else {
-            // -------- B job: 16 consecutive columns n = 16 t + col, col = kappa + 4 n'' --------
+            // -------- B job: NCOL consecutive columns n = NCOL t + col, col = kappa + 4 n'' --------
             const int t = job;
-            // tile chunk layout: chunk (kap, hf) holds n'' = 2hf, 2hf+1 -> logical col index
-            // used by tile_pos is cl = 2*(2 kap + hf) + (n'' & 1)
             const int kap = warp & 3, nn = warp >> 2;
-            const int cl = 2 * (2 * kap + (nn >> 1)) + (nn & 1);
-            C v[EM];
-#pragma unroll
-            for (int kk = 0; kk < EM; ++kk) v[kk] = tile[tile_pos(lane + 32 * kk, cl)];
-            __syncthreads();  // tile consumed
-            issued = false;
-            if (can_pf) { issue_tile<T, D, MM, Q>(tile, A, ws, w2, isA2, job2); issued = true; }
-            fM.run(v, scr, lane);
-            C* Out = uni;
-            const int n = 16 * t + warp;   // warp = kappa + 4 n''
+            const int cl = 2 * (kap * (Cfg::NPK / 2) + (nn >> 1)) + (nn & 1);
+            const int n = NCOL * t + warp;   // warp = kappa + 4 n''
             const C e = __ldg((const C*)A.E + n);
             const int rt = __ldg(A.rot + n);
-            const int k1 = lane % EM, jo = WarpFft<T, EM>::out_jo(lane);
+            C v[EM];
 #pragma unroll
-            for (int kk = 0; kk < EM; ++kk) {
-                const int m = k1 + EM * kk + EM * EM * jo;
-                const int mo = (m - rt) & (MM - 1);
-                Out[mo * 16 + (warp ^ (mo & 15))] = cmul(e, v[kk]);
-            }
+            for (int kk = 0; kk < EM; ++kk) v[kk] = tile[tile_pos<NCOL>(lane + 32 * kk, cl)];
+            __syncthreads();  // tile consumed
+            issued = false;
+            if (can_pf) { issue_tile<T, D, MM, Q, NCOL>(tile, A, ws, w2, isA2, job2); issued = true; }
+            if (!(A.dbg & 2)) fM.run(v, scr, lane);
+            C* Out = uni;
+            if (tid == 0) bulk_wait_read0();   // the previous output box has left uni
             __syncthreads();
-            C* cw = (C*)A.out + w * MM * A.N + 16 * t;
-            constexpr int PER2 = MM * 8 / NT;
+            const int k1 = lane % EM, jo = WarpFft<T, EM>::out_jo(lane);
+            if (NCOL == 16 && A.tma) {
+                // TMA SWIZZLE_128B layout: row mo = 128 B, 16-byte chunk index XOR (mo & 7)
 #pragma unroll
-            for (int i = 0; i < PER2; ++i) {
-                const int e2 = tid + NT * i;
-                const int mo = e2 >> 3, pp = e2 & 7, sw = mo & 15;
-                float4 val = *(const float4*)(Out + mo * 16 + 2 * (pp ^ (sw >> 1)));
-                if (sw & 1) val = make_float4(val.z, val.w, val.x, val.y);
-                __stcs((float4*)(cw + (int64_t)mo * A.N + 2 * pp), val);
+                for (int kk = 0; kk < EM; ++kk) {
+                    const int m = k1 + EM * kk + EM * EM * jo;
+                    const int mo = (m - rt) & (MM - 1);
+                    Out[mo * 16 + ((((warp >> 1) ^ (mo & 7)) << 1) | (warp & 1))] = cmul(e, v[kk]);
+                }
+                fence_proxy_async_smem();
+                __syncthreads();
+                if (tid == 0 && !(A.dbg & 8)) {
+#pragma unroll
+                    for (int bx = 0; bx < MM / 256; ++bx)
+                        tma_store_2d(&cmap, Out + bx * 256 * 16, 32 * t, (int)(w * MM) + 256 * bx);
+                    bulk_commit();
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < EM; ++kk) {
+                    const int m = k1 + EM * kk + EM * EM * jo;
+                    const int mo = (m - rt) & (MM - 1);
+                    const int x = NCOL == 16 ? (mo & 15) : ((mo >> 1) & 7);
+                    Out[mo * NCOL + (warp ^ x)] = cmul(e, v[kk]);
+                }
+                __syncthreads();
+                C* cw = (C*)A.out + w * MM * A.N + NCOL * t;
+                constexpr int VPR = NCOL / 2;               // float4 per output row
+                constexpr int PER2 = MM * VPR / NT;
+#pragma unroll
+                for (int i = 0; i < PER2; ++i) {
+                    const int e2 = tid + NT * i;
+                    const int mo = e2 / VPR, pp = e2 % VPR;
+                    const int x = NCOL == 16 ? (mo & 15) : ((mo >> 1) & 7);
+                    float4 val = *(const float4*)(Out + mo * NCOL + 2 * (pp ^ (x >> 1)));
+                    if (x & 1) val = make_float4(val.z, val.w, val.x, val.y);
+                    if (!(A.dbg & 8)) __stcs((float4*)(cw + (int64_t)mo * A.N + 2 * pp), val);
+                }
             }
         }
         ++k;
         have = more;
         if (have) { w = w2; isA = isA2; job = job2; }
     }
-    // finish this CTA's remaining barriers (its last signal's phases)
-    while (cur_w < A.W) {
+    while (cur_w < A.W) {   // this CTA's remaining barriers
         group_barrier(bar, (++epoch) * A.GS);
         if (phase == 0) phase = 1; else { phase = 0; cur_w += A.ngroups; }
     }
     cp_async_wait_all();
+    if (tid == 0) bulk_wait0();
 }
 
 // ------------------------------------------------------------------------------------
 // plan-side glue
 // ------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
 struct FastPlan {
     int kind = 0;  // 0 = none (generic path); 1 = fused T-branch p=1
     const char* name = "none";
     int D = 0, MM = 0, Q = 0, c = 0, N = 0;
     int64_t L = 0;
-    int nA = 0, nB = 0, GS = 16, ngroups = 1;
+    int nA = 0, nB = 0, GS = 16, ngroups = 1, ncol = 16;
     int grid = 0;
     size_t smem = 0;
     size_t esz = 8;
@@ -447,15 +519,16 @@ struct FastPlan {
     const void* E = nullptr;
     const int* rot = nullptr;
     int* counters = nullptr;
-    void (*launch)(const FusedArgs&, int grid, size_t smem, cudaStream_t, const cudaAccessPolicyWindow*) = nullptr;
+    void (*launch)(const FusedArgs&, const CUtensorMap&, int grid, size_t smem, cudaStream_t, const cudaAccessPolicyWindow*) = nullptr;
     bool persist = false;   // L2 persisting window over the intermediate workspace
 };
 
-template <typename T, int D, int MM, int Q>
-void launch_fused(const FusedArgs& a, int grid, size_t smem, cudaStream_t st, const cudaAccessPolicyWindow* apw) {
+template <typename T, int D, int MM, int Q, int NCOL>
+void launch_fused(const FusedArgs& a, const CUtensorMap& cmap, int grid, size_t smem, cudaStream_t st,
+                  const cudaAccessPolicyWindow* apw) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(FusedCfg<T, D, MM, Q>::NTHR);
+    cfg.blockDim = dim3(FusedCfg<T, D, MM, Q, NCOL>::NTHR);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -468,7 +541,7 @@ void launch_fused(const FusedArgs& a, int grid, size_t smem, cudaStream_t st, co
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, fused_t_kernel<T, D, MM, Q>, a);
+    cudaLaunchKernelEx(&cfg, fused_t_kernel<T, D, MM, Q, NCOL>, a, cmap);
 }
 
 template <typename T>
@@ -490,22 +563,23 @@ __global__ void k_chirp_factors(cx<T>* Cj, cx<T>* Rs, int64_t K, int64_t L, int6
     }
 }
 
-template <typename T, int D, int MM, int Q>
+template <typename T, int D, int MM, int Q, int NCOL>
 static int setup_fused(FastPlan* fp) {
-    using Cfg = FusedCfg<T, D, MM, Q>;
+    using Cfg = FusedCfg<T, D, MM, Q, NCOL>;
     fp->smem = Cfg::SMEM;
-    if (cudaFuncSetAttribute(fused_t_kernel<T, D, MM, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fp->smem) !=
+    if (cudaFuncSetAttribute(fused_t_kernel<T, D, MM, Q, NCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fp->smem) !=
         cudaSuccess)
         return DGT_ECUDA;
     int per_sm = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_t_kernel<T, D, MM, Q>, 512, fp->smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_t_kernel<T, D, MM, Q, NCOL>, Cfg::NTHR, fp->smem) !=
             cudaSuccess ||
         per_sm < 1)
         return DGT_EUNSUPPORTED;
     fp->grid = per_sm * sms;
-    fp->launch = &launch_fused<T, D, MM, Q>;
+    fp->launch = &launch_fused<T, D, MM, Q, NCOL>;
+    fp->ncol = NCOL;
     return DGT_OK;
 }
 
@@ -519,16 +593,17 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, void* G, void* /*chirp*/
     const int64_t D = I.d, MM = I.iM;
     int rc = DGT_OK;
     if constexpr (std::is_same<T, float>::value) {
-        if (D == 512 && MM == 512) rc = setup_fused<T, 512, 512, 4>(fp);
-        else if (D == 256 && MM == 256) rc = setup_fused<T, 256, 256, 4>(fp);
+        const int ncol = std::getenv("NSDGT_NCOL") ? std::atoi(std::getenv("NSDGT_NCOL")) : 16;
+        if (D == 512 && MM == 512) rc = ncol == 16 ? setup_fused<T, 512, 512, 4, 16>(fp) : setup_fused<T, 512, 512, 4, 8>(fp);
+        else if (D == 256 && MM == 256) rc = ncol == 16 ? setup_fused<T, 256, 256, 4, 16>(fp) : setup_fused<T, 256, 256, 4, 8>(fp);
         else return DGT_OK;
     } else {
         return DGT_OK;  // c128 uses the generic kernels (round 1)
     }
     if (rc) return DGT_OK;  // fall back to the generic kernels (still CUDA)
     fp->D = (int)D; fp->MM = (int)MM; fp->Q = (int)I.q; fp->c = (int)I.c; fp->N = (int)I.N; fp->L = I.L;
-    fp->nA = (int)(I.c / 4);   // 16 columns (4 residues x 4 l) per A job
-    fp->nB = (int)(D / 4);     // 16 consecutive columns n per B job
+    fp->nA = (int)(I.c / 4) * (16 / fp->ncol);   // ncol columns (4 residues x ncol/4 l) per A job
+    fp->nB = (int)(D * 4 / fp->ncol);            // ncol consecutive columns n per B job
     // groups of GS CTAs each own one signal at a time; the intermediates of the signals in
     // flight (ngroups x per-signal bytes) must stay L2 resident
     {
@@ -595,7 +670,29 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
     apw.hitRatio = 1.0f;
     apw.hitProp = cudaAccessPropertyPersisting;
     apw.missProp = cudaAccessPropertyStreaming;
-    fp->launch(a, fp->GS * fp->ngroups, fp->smem, st, fp->persist ? &apw : nullptr);
+    // TMA descriptor of the output c viewed as W*M rows x 2N floats (box: 128 B x 256 rows)
+    CUtensorMap cmap;
+    std::memset(&cmap, 0, sizeof cmap);
+    a.tma = fp->ncol == 16 && std::getenv("NSDGT_TMA") != nullptr;
+    a.discard = std::getenv("NSDGT_DISCARD") != nullptr;
+    if (a.tma) {
+        static PFN_encodeTiled encode = nullptr;
+        if (!encode) {
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+                !encode)
+                return DGT_ECUDA;
+        }
+        cuuint64_t gdim[2] = {(cuuint64_t)2 * fp->N, (cuuint64_t)W * fp->MM};
+        cuuint64_t gstr[1] = {(cuuint64_t)2 * fp->N * sizeof(float)};
+        cuuint32_t box[2] = {32, 256};
+        cuuint32_t est[2] = {1, 1};
+        if (encode(&cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, c, gdim, gstr, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return DGT_ECUDA;
+    }
+    fp->launch(a, cmap, fp->GS * fp->ngroups, fp->smem, st, fp->persist ? &apw : nullptr);
     return DGT_OK;
 }
 
