@@ -34,8 +34,12 @@
 #include "../../include/nsdgt.h"
 #include "cplx.cuh"
 #include "fft_smem.cuh"
+#include "fused7.cuh"
 
 namespace nsdgt {
+
+template <typename T>
+__global__ void k_window_factor(cx<T>* G, const double2* gt, int64_t L, int64_t c, int64_t d, int64_t p, int64_t q);
 
 // ------------------------------------------------------------------------------------
 // warp FFT, N = 32*E, forward (exp(-2 pi i jk/N))
@@ -521,6 +525,9 @@ struct FastPlan {
     int* counters = nullptr;
     void (*launch)(const FusedArgs&, const CUtensorMap&, int grid, size_t smem, cudaStream_t, const cudaAccessPolicyWindow*) = nullptr;
     bool persist = false;   // L2 persisting window over the intermediate workspace
+    // kind 2 (fused7): per-column window table G', ring of S7 slots, look-ahead lag7
+    void* Gp7 = nullptr;
+    int beta7 = 0, S7 = 6, lag7 = 4;
 };
 
 template <typename T, int D, int MM, int Q, int NCOL>
@@ -639,11 +646,14 @@ inline void free_fast(FastPlan* fp) {
     if (fp->Cj) cudaFree(fp->Cj);
     if (fp->Rs) cudaFree(fp->Rs);
     if (fp->counters) cudaFree(fp->counters);
+    if (fp->Gp7) cudaFree(fp->Gp7);
+    fp->Gp7 = nullptr;
     fp->Cj = fp->Rs = nullptr;
     fp->counters = nullptr;
 }
 
 inline size_t fast_workspace_bytes(const FastPlan* fp, int64_t /*Wc*/) {
+    if (fp->kind == 2) return (size_t)fp->S7 * fp->MM * fp->Q * fp->D * fp->esz;
     return (size_t)fp->ngroups * fp->MM * fp->Q * fp->D * fp->esz;
 }
 
@@ -651,9 +661,141 @@ inline size_t fast_workspace_bytes(const FastPlan* fp, int64_t /*Wc*/) {
 inline int64_t fast_chunk(const FastPlan*) { return (int64_t)1 << 40; }
 inline int64_t fast_launches_per_chunk(const FastPlan*) { return 1; }
 
+template <int D>
+static void launch7(const v7::Args& a, int grid, size_t smem, cudaStream_t st, const cudaAccessPolicyWindow* apw) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(v7::Cfg<D>::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    int na = 0;
+    if (apw) {
+        // keep the intermediate ring L2 resident while f and c stream through
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow = *apw;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, v7::fused7_kernel<D>, a);
+}
+
+// kind 2: the fused7 kernel (fused7.cuh).  Builds G' from the fp64 window factors and checks,
+// on the host, the identities the kernel relies on; returns DGT_OK with
+// fp->kind unchanged when the lattice does not qualify.
+template <typename T>
+int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const void* E, cudaStream_t st) {
+    if constexpr (!std::is_same<T, float>::value) return DGT_OK;
+    if (std::getenv("NSDGT_V6")) return DGT_OK;
+    if (I.branch == DGT_BRANCH_FREQ || I.p != 1 || I.q != 4 || I.d != I.iM || (I.d != 512 && I.d != 256)) return DGT_OK;
+    if (I.c % 16 != 0 || I.N % (16 * v7::Cfg<512>::BT) != 0 || I.iM != I.M) return DGT_OK;
+    const int64_t L = I.L, twoL = 2 * L, D = I.d, M = I.M, Q = I.q, N = I.N;
+    const int64_t sigma = ((I.chirp_sigma % twoL) + twoL) % twoL;
+    const int64_t K = (int64_t)((unsigned __int128)sigma * (unsigned __int128)((L + 1) % twoL) % (unsigned __int128)twoL);
+    if (((unsigned __int128)K * ((unsigned __int128)M * M % twoL)) % twoL != 0) return DGT_OK;  // R(s) == 1 required
+    // rotation identity rot(n(tau)) = alpha_{l,u} - beta tau (mod M), n(tau) = (l - u - q tau) mod N
+    if ((I.s1 * I.a * Q) % I.b != 0) return DGT_OK;
+    const int64_t beta = ((I.s1 * I.a * Q / I.b) % M + M) % M;
+    auto rotm = [&](int64_t n) {
+        const __int128 x = (__int128)I.s1 * I.a * n;
+        const int64_t r = (int64_t)(((x + I.b - 1) / I.b) % M);
+        return ((r % M) + M) % M;
+    };
+    v7::GpArgs ga{};
+    for (int l = 0; l < Q; ++l)
+        for (int u = 0; u < Q; ++u) {
+            const int64_t alpha = rotm((((l - u) % N) + N) % N);
+            ga.alpha[l * Q + u] = (int)alpha;
+            for (int64_t tau = 0; tau < D; ++tau) {
+                const int64_t n = (((l - u - Q * tau) % N) + N) % N;
+                if (rotm(n) != (((alpha - beta * tau) % M) + M) % M) return DGT_OK;
+            }
+        }
+    // fp64 window factors G64[(r q + u) d + nu] = conj(Gamma)/d, then G'
+    double2* G64 = nullptr;
+    if (cudaMalloc(&G64, sizeof(double2) * L) != cudaSuccess) return DGT_ENOMEM;
+    k_window_factor<double><<<(unsigned)std::min<int64_t>((L + 255) / 256, 148 * 64), 256, 0, st>>>(G64, gt, L, I.c, I.d, 1, Q);
+    const size_t gp_bytes = sizeof(float2) * (size_t)M * Q * D;
+    if (cudaMalloc(&fp->Gp7, gp_bytes) != cudaSuccess) { cudaFree(G64); return DGT_ENOMEM; }
+    ga.Gp = (float4*)fp->Gp7; ga.G64 = G64; ga.L = L; ga.K = K;
+    ga.M = (int)M; ga.D = (int)D; ga.Q = (int)Q; ga.c = (int)I.c; ga.beta = (int)beta; ga.R1 = (int)(D / 16);
+    v7::k_gprime<<<(unsigned)std::min<int64_t>((M * Q * D + 255) / 256, 148 * 64), 256, 0, st>>>(ga);
+    if (cudaStreamSynchronize(st) != cudaSuccess) { cudaFree(G64); return DGT_ECUDA; }
+    cudaFree(G64);
+    size_t smem = D == 512 ? v7::Cfg<512>::SMEM : v7::Cfg<256>::SMEM;
+    auto kfn = D == 512 ? (const void*)v7::fused7_kernel<512> : (const void*)v7::fused7_kernel<256>;
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return DGT_ECUDA;
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem) != cudaSuccess || per_sm < 1)
+        return DGT_EUNSUPPORTED;
+    fp->grid = per_sm * sms;
+    fp->smem = smem;
+    fp->D = (int)D; fp->MM = (int)M; fp->Q = (int)Q; fp->c = (int)I.c; fp->N = (int)N; fp->L = L;
+    fp->nA = (int)(M / v7::Cfg<512>::ACOL); fp->nB = (int)(N / (16 * v7::Cfg<512>::BT));
+    fp->Kmod = (int)(K % D);
+    fp->beta7 = (int)beta;
+    if (const char* e = std::getenv("NSDGT_S")) fp->S7 = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("NSDGT_LAG")) fp->lag7 = std::max(0, std::atoi(e));
+    if (fp->lag7 >= fp->S7) fp->lag7 = fp->S7 - 1;
+    fp->E = E;
+    fp->esz = sizeof(float2);
+    // L2 set-aside for the ring (NSDGT_PERSIST=0 disables): a persisting access-policy window
+    fp->persist = false;
+    {
+        const char* e = std::getenv("NSDGT_PERSIST");
+        int maxp = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        const size_t ring = (size_t)fp->S7 * M * Q * D * sizeof(float2);
+        if (!(e && e[0] == '0') && maxp > 0) {
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t want = std::min<size_t>((size_t)maxp, ring);
+            if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            fp->persist = true;
+        }
+        cudaGetLastError();
+    }
+    fp->kind = 2;
+    fp->name = "fused7_t_p1";
+    return DGT_OK;
+}
+
 template <typename T>
 int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int64_t W, cudaStream_t st) {
     if (real_in) return DGT_EUNSUPPORTED;
+    if (fp->kind == 2) {
+        const int nctr = 1 + 2 * fp->S7;
+        if (!fp->counters) {
+            if (cudaMalloc(&fp->counters, sizeof(int) * nctr) != cudaSuccess) return DGT_ENOMEM;
+        }
+        if (cudaMemsetAsync(fp->counters, 0, sizeof(int) * nctr, st) != cudaSuccess) return DGT_ECUDA;
+        v7::Args a{};
+        a.f = (const float2*)f; a.out = (float2*)c; a.ws = (float2*)ws; a.Gp = (const float4*)fp->Gp7;
+        if (W * (int64_t)(fp->nA + fp->nB) >= (int64_t)1 << 31) return DGT_EUNSUPPORTED;
+        a.E = (const float2*)fp->E; a.ctr = fp->counters; a.W = (int)W; a.N = fp->N; a.c = fp->c; a.Kmod = fp->Kmod;
+        a.dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;
+        if (a.dbg & 16) {
+            static unsigned long long* logbuf = nullptr;
+            if (!logbuf) cudaMalloc(&logbuf, sizeof(unsigned long long) * 8 * 4096);
+            cudaMemsetAsync(logbuf, 0, sizeof(unsigned long long) * 8 * 4096, st);
+            a.log = logbuf;
+            if (const char* e = std::getenv("NSDGT_LOGPTR")) *(unsigned long long**)std::strtoull(e, nullptr, 10) = logbuf;
+        }
+        a.beta = fp->beta7; a.S = fp->S7; a.lag = fp->lag7; a.nA = fp->nA; a.nB = fp->nB;
+        cudaAccessPolicyWindow apw{};
+        apw.base_ptr = ws;
+        apw.num_bytes = fast_workspace_bytes(fp, W);
+        apw.hitRatio = 1.0f;
+        apw.hitProp = cudaAccessPropertyPersisting;
+        apw.missProp = cudaAccessPropertyStreaming;
+        const cudaAccessPolicyWindow* pw = fp->persist ? &apw : nullptr;
+        if (fp->D == 512) launch7<512>(a, fp->grid, fp->smem, st, pw);
+        else launch7<256>(a, fp->grid, fp->smem, st, pw);
+        return DGT_OK;
+    }
     if (!fp->counters) {
         if (cudaMalloc(&fp->counters, sizeof(int) * fp->ngroups) != cudaSuccess) return DGT_ENOMEM;
     }

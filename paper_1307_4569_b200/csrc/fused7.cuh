@@ -1,0 +1,550 @@
+// fused7.cuh -- the round-1 hot-path kernel for the time-shear / separable branch with
+// p = 1, q = 4, d = M in {256, 512}, complex64 (BASELINE configs 3 and 5).  DESIGN.md §4.3.
+//
+// Notation (Alg. 1 of PAPER.md:852-873, factorisation PAPER.md:790-804):
+// x = j + s M (j < M, s < D = d), j = r + c l, n = kappa + q n'.  With the chirp
+// factorisation P_sigma(j + sM) = C(j) W_D^{-sh_j s} (R(s) == 1 is required here) and the
+// Alg. 1 row rotation rot(n(tau)) = alpha_{l,u} - beta tau (mod M) for n(tau) = (l-u-q tau)
+// mod N, the whole T-branch reduces to two batched D-point DFT passes per signal:
+//
+//   pass A, column j:  F_j(mu) = sum_s f(j + sM) W_D^{s mu}                      (Zak DFT)
+//                      for u < q:  x_{j,u}(mu) = F_j((sigma_j - mu) mod D) G'_{j,u}(mu)
+//                                  ws[j][kappa][n'] = DFT_D[x_{j,u}](n'),  kappa = (l-u) mod q
+//   pass B, column n:  c[m][n] = E(n) sum_j ws[j][n mod q][n div q] W_M^{j m}
+//
+// sigma_j = (j beta - sh_j) mod D, and the plan-time table
+//   G'_{j,u}(mu) = G_{r,u}((j beta - mu) mod D) C(j) W_D^{j alpha_{l,u}} W_D^{-mu e_{l,u}},
+//   e_{l,u} = floor((l-u)/q),  G = conj(Gamma)/d  (the window factorisation)
+// carries the window, the column chirp C(j), the Alg. 1 row rotation and the output
+// index reversal, so ws is already rotated: pass B needs only E(n).  (Derivation:
+// DESIGN.md §4.3; every identity is exact, the table is built in fp64.)
+//
+// Execution: one persistent launch, CTAs of 256 threads pull jobs from a global queue.
+//   A job = 8 consecutive columns j of one signal (1 Zak DFT + q product DFTs each),
+//   B job = 16 consecutive columns n (1 DFT over j each).
+// Dependencies (B(w) after all A(w); A(w) after all B(w - S) because it reuses ring slot
+// w mod S) are per-slot monotone counters; every job a CTA waits on was dequeued earlier
+// by a resident CTA, so the spin cannot deadlock.
+//
+// The D-point DFT of a 16-column tile: D = 16 R1, index x = t + 16 k.  Lane (col, t)
+// holds x(t + 16k), k < R1, loaded straight from global memory (16 columns of a row are
+// 128 contiguous bytes); it runs a register DFT-R1 over k and multiplies W_D^{t m1}.  One
+// shared-memory exchange (in rounds of 16 values of m1 to halve the buffer) gives each
+// lane whole sequences over t; a register DFT-16 finishes X(m1 + R1 m2).  All complex
+// arithmetic is packed FP32x2 (FADD2/FFMA2/FMUL2): one instruction per complex add, two
+// per complex multiply.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cplx.cuh"
+
+namespace nsdgt {
+namespace v7 {
+
+// ------------------------------------------------------------------------------------
+// packed FP32x2 complex arithmetic
+// ------------------------------------------------------------------------------------
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float2 a) {
+    u64 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 upk(u64 r) {
+    float2 v;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+    return upk(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+// a + (-i) b
+__device__ __forceinline__ float2 cadd_mi(float2 a, float2 b) { return fma2(make_float2(b.y, b.x), make_float2(1.f, -1.f), a); }
+// a - (-i) b
+__device__ __forceinline__ float2 csub_mi(float2 a, float2 b) { return fma2(make_float2(b.y, b.x), make_float2(-1.f, 1.f), a); }
+// d * w  (FMUL2 + FFMA2)
+__device__ __forceinline__ float2 cmw(float2 d, float2 w) {
+    return fma2(make_float2(-d.y, d.x), make_float2(w.y, w.y), mul2(d, make_float2(w.x, w.x)));
+}
+// d * (-i)
+__device__ __forceinline__ float2 cmi(float2 d) { return make_float2(d.y, -d.x); }
+
+// W_32^k = exp(-2 pi i k / 32), k < 32
+__device__ __forceinline__ float2 w32(int k) {
+    constexpr float cs[8] = {1.0f, 0.98078528040323044913f, 0.92387953251128675613f, 0.83146961230254523708f,
+                             0.70710678118654752440f, 0.55557023301960222474f, 0.38268343236508977173f,
+                             0.19509032201612826785f};
+    // cos(2 pi k/32) for k in [0,8] via symmetry
+    const int q = k >> 3, r = k & 7;
+    float c, s;  // cos, sin of 2 pi k / 32
+    if (q == 0) { c = cs[r]; s = r ? cs[8 - r] : 0.f; }
+    else if (q == 1) { c = r ? -cs[8 - r] : 0.f; s = cs[r]; }
+    else if (q == 2) { c = -cs[r]; s = r ? -cs[8 - r] : 0.f; }
+    else { c = r ? cs[8 - r] : 0.f; s = -cs[r]; }
+    return make_float2(c, -s);
+}
+
+// ------------------------------------------------------------------------------------
+// register DFTs (forward, natural order in and out; all indices compile-time)
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void dft4(float2& v0, float2& v1, float2& v2, float2& v3) {
+    const float2 t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = csub(v1, v3);
+    v0 = cadd(t0, t2);
+    v2 = csub(t0, t2);
+    v1 = cadd_mi(t1, t3);
+    v3 = csub_mi(t1, t3);
+}
+
+// X[k1 + 4 k2] = sum_{n1} W16^{n1 k1} W4^{n1 k2} sum_{n2} x[n1 + 4 n2] W4^{n2 k1}
+__device__ __forceinline__ void dft16(float2* v) {
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) dft4(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);
+    // v[n1 + 4 k1] *= W16^{n1 k1} = W32^{2 n1 k1}
+    v[5] = cmw(v[5], w32(2));
+    v[9] = cmw(v[9], w32(4));
+    v[13] = cmw(v[13], w32(6));
+    v[6] = cmw(v[6], w32(4));
+    v[10] = cmi(v[10]);
+    v[14] = cmw(v[14], w32(12));
+    v[7] = cmw(v[7], w32(6));
+    v[11] = cmw(v[11], w32(12));
+    v[15] = cmw(v[15], w32(18));
+    float2 y[16];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        float2 a0 = v[4 * k1], a1 = v[4 * k1 + 1], a2 = v[4 * k1 + 2], a3 = v[4 * k1 + 3];
+        dft4(a0, a1, a2, a3);
+        y[k1] = a0; y[k1 + 4] = a1; y[k1 + 8] = a2; y[k1 + 12] = a3;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = y[i];
+}
+
+// radix-2 DIT: E = DFT16(even), O = DFT16(odd); X[k] = E + W32^k O, X[k+16] = E - W32^k O
+__device__ __forceinline__ void dft32(float2* v) {
+    float2 e[16], o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { e[i] = v[2 * i]; o[i] = v[2 * i + 1]; }
+    dft16(e);
+    dft16(o);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k == 0) { v[0] = cadd(e[0], o[0]); v[16] = csub(e[0], o[0]); }
+        else if (k == 8) { v[8] = cadd_mi(e[8], o[8]); v[24] = csub_mi(e[8], o[8]); }
+        else {
+            const float2 t = cmw(o[k], w32(k));
+            v[k] = cadd(e[k], t);
+            v[k + 16] = csub(e[k], t);
+        }
+    }
+}
+
+template <int R> __device__ __forceinline__ void dftR(float2* v) {
+    if constexpr (R == 16) dft16(v);
+    else dft32(v);
+}
+
+// ------------------------------------------------------------------------------------
+// kernel arguments and job queue
+// ------------------------------------------------------------------------------------
+struct Args {
+    const float2* f;     // [W][L]
+    float2* out;         // [W][M][N]
+    float2* ws;          // [S][M][Q][D]
+    const float4* Gp;    // G' [M][Q][R1/2][16] of float4 (pairs k, k+1)
+    const float2* E;     // [N]
+    int* ctr;            // [0] job queue, [1..S] doneA per slot, [1+S..2S] doneB per slot
+    int W, N, c, Kmod, beta;
+    int S, lag, nA, nB;
+    unsigned long long* log;   // dbg & 16: per-CTA phase timestamps (CTAs < 8, 4096 entries each)
+    int dbg;             // experiment knobs (0 in production): 1 no dependency spin, 2 no global loads,
+                         // 4 no global stores, 8 no DFT arithmetic
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void spin_until(const int* p, int target) {
+    if (ld_acquire(p) >= target) return;
+    while (ld_acquire(p) < target) __nanosleep(64);
+}
+__device__ __forceinline__ float2 ld_cs(const float2* p) { return __ldcs(p); }
+__device__ __forceinline__ float2 ld_cg(const float2* p) { return __ldcg(p); }
+
+// job p -> (isA, w, idx): blocks g = 0, 1, ...: A(g) jobs (g < W) then B(g - lag) jobs (g >= lag).
+// 32-bit arithmetic (the host checks W (nA + nB) < 2^31).
+__device__ __forceinline__ bool decode(int p, int W, int lag, int nA, int nB, int* isA, int* w, int* idx) {
+    const int lagE = lag < W ? lag : W;
+    const int seg1 = lagE * nA, seg2 = (W - lagE) * (nA + nB), seg3 = lagE * nB;
+    if (p < seg1) { *isA = 1; *w = p / nA; *idx = p - *w * nA; return true; }
+    p -= seg1;
+    if (p < seg2) {
+        const int t = p / (nA + nB), r = p - t * (nA + nB);
+        if (r < nA) { *isA = 1; *w = lagE + t; *idx = r; }
+        else { *isA = 0; *w = t; *idx = r - nA; }
+        return true;
+    }
+    p -= seg2;
+    if (p < seg3) { const int t = p / nB; *isA = 0; *w = W - lagE + t; *idx = p - t * nB; return true; }
+    return false;
+}
+
+template <int D>
+struct Cfg {
+    static constexpr int R1 = D / 16;            // stage-1 length (32 or 16)
+    static constexpr int NR = R1 / 16;           // stage-2 sequences per lane (2 or 1)
+    static constexpr int Q = 4;
+    static constexpr int NT = 256;               // 16 column slots x 16 lanes
+    static constexpr int ACOL = 8;               // columns j per A job
+    static constexpr int BT = 1;                 // 16-column tiles per B job
+    static constexpr int XE = 16 * D;            // exchange buffer, complex (16 slots x D)
+    static constexpr int FE = ACOL * D;          // F buffer, complex
+    static constexpr int TW = 16 * 16;           // twiddle table W_D^{t m}, t, m < 16
+    static constexpr size_t SMEM = (size_t)(XE + FE + TW) * 8;
+};
+
+// Exchange buffer, 8-byte slots: slot(col, m1, t) = col*D + m1*16 + (t ^ f(col, m1)),
+// f = (m1 + g(col)) & 15, g(c) = 8 (c & 1) + 2 ((c >> 1) & 3) + (c >> 3) (a permutation of
+// 0..15).  Stage-2 lane i reads sequences m1 = 16 r + i.  Every half-warp access of the
+// thread-role maps below hits 16 distinct bank pairs (tools/bank_check.py).
+template <int D>
+__device__ __forceinline__ int xs(int col, int m1, int t) {
+    const int g = 8 * (col & 1) + 2 * ((col >> 1) & 3) + (col >> 3);
+    return col * D + m1 * 16 + (t ^ ((m1 + g) & 15));
+}
+
+// Stage 1 -> exchange -> stage 2 of a 16-slot D-point DFT tile.
+//   in:  v[k] = x(t + 16 k) of slot s1col, lane t
+//   out: emit(r, y) for r < NR, y[m2] = X(16 r + oi + R1 m2) of slot ocol
+// The writer applies W_D^{t (m1 mod 16)} (table row tw = W_D^{t *}); the reader of
+// sequence m1 = 16 + i applies the rest, W_D^{16 t} = W_32^t (compile-time constants).
+// before_sync() runs after this thread's exchange writes, after_sync() right after the
+// barrier (v is dead by then: the caller may refill its prefetch registers).  Leaves the
+// exchange buffer busy: the caller must __syncthreads before the next write.  Warps that
+// sit a tile out call dft_tile_idle (the same single barrier; warp-uniform branch).
+template <int D, class Before, class After, class Emit, class Mark>
+__device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2, int s1col, int t, int ocol, int oi,
+                                         Before&& before_sync, After&& after_sync, Emit&& emit, int dbg, Mark&& mark) {
+    constexpr int R1 = Cfg<D>::R1, NR = Cfg<D>::NR;
+    mark(10);
+    if (!(dbg & 8)) dftR<R1>(v);
+    mark(11);
+#pragma unroll
+    for (int m = 0; m < R1; ++m) {
+        const float2 val = (m & 15) ? cmw(v[m], tw[m & 15]) : v[m];
+        X2[xs<D>(s1col, m, t)] = val;
+        if ((m & 7) == 7) asm volatile("" ::: "memory");   // bound the twiddle loads in flight
+    }
+    before_sync();
+    mark(12);
+    __syncthreads();
+    mark(13);
+    after_sync();
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        float2 y[16];
+#pragma unroll
+        for (int tt = 0; tt < 16; ++tt) y[tt] = X2[xs<D>(ocol, 16 * r + oi, tt)];
+        if (r == 1) {
+#pragma unroll
+            for (int tt = 1; tt < 16; ++tt) y[tt] = cmw(y[tt], w32(tt));
+        }
+        if (!(dbg & 8)) dft16(y);
+        emit(r, y);
+    }
+    mark(14);
+}
+__device__ __forceinline__ void dft_tile_idle() { __syncthreads(); }
+
+template <int D>
+__global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
+    using K = Cfg<D>;
+    constexpr int R1 = K::R1, Q = K::Q, M = D, AC = K::ACOL, BT = K::BT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* X2 = reinterpret_cast<float2*>(smem_raw);
+    float2* F = X2 + K::XE;        // F[col][nu ^ 2 col], col < ACOL
+    float2* twt = F + K::FE;       // twt[t][m] = W_D^{t m}
+    __shared__ int jobsm[2];       // next job, 1 if its first tile's inputs were prefetched
+    const int tid = threadIdx.x;
+    // thread-role maps (t = stage-1 lane index, i = stage-2 lane index):
+    //   S1_16 / M1_16: slot c16 = tid & 15, t / i = h16 = tid >> 4
+    //   S1_8  / M1_8 : col  c8  = tid & 7,  t / i = h8  = tid >> 3   (tid < 128)
+    //   M3 (u-tiles) : warp w, lane L: slot 4 (w >> 1) + (L >> 3), i = (L & 7) + 8 (w & 1)
+    const int c16 = tid & 15, h16 = tid >> 4, c8 = tid & 7, h8 = (tid >> 3) & 15;
+    for (int e = tid; e < K::TW; e += K::NT) {
+        const int tt = e / 16, m = e % 16;
+        double s, c;
+        sincospi(-2.0 * (double)((tt * m) % D) / (double)D, &s, &c);
+        twt[e] = make_float2((float)c, (float)s);
+    }
+    unsigned long long* lg = (A.dbg & 16) && blockIdx.x < 8 && tid == 0 ? A.log + (size_t)blockIdx.x * 4096 : nullptr;
+    int nlog = 0;
+    auto mark = [&](int code) {
+        if (lg && nlog < 4095) lg[nlog++] = (gtimer() << 8) | (unsigned long long)code;
+    };
+    int* queue = A.ctr;
+    int* doneA = A.ctr + 1;
+    int* doneB = A.ctr + 1 + A.S;
+    const int64_t MQD = (int64_t)M * Q * D;
+
+    // ---- global inputs of a tile, loaded into pre[] (this thread's role) ----
+    float2 pre[R1];
+    auto load_f = [&](int w, int j0) {          // Zak DFT input (role S1_8, tid < 128)
+        const float2* fw = A.f + (int64_t)w * M * D + j0 + c8;
+#pragma unroll
+        for (int k = 0; k < R1; ++k) pre[k] = ld_cs(fw + (int64_t)(h8 + 16 * k) * M);
+    };
+    // G' of u-tile h (role S1_16: slot c16 = 4 col + u, lane t): values k in [16 b, 16 b + 16).
+    // Layout [j0 / 8][h][kp][t][slot] of float4 (k = 2 kp, 2 kp + 1): a half-warp reads 256
+    // contiguous bytes.
+    auto load_g = [&](int j0, int h, int b) {
+        const float4* G4 = A.Gp + ((int64_t)((j0 / AC) * 2 + h) * (R1 / 2)) * 256 + h16 * 16 + c16;
+#pragma unroll
+        for (int kp = 8 * b; kp < 8 * b + 8 && kp < R1 / 2; ++kp) {
+            const float4 g = __ldg(G4 + kp * 256);
+            pre[2 * kp] = make_float2(g.x, g.y);
+            pre[2 * kp + 1] = make_float2(g.z, g.w);
+        }
+    };
+    auto load_ring = [&](int w, int idx) {      // pass-B input (role S1_16): line (j, idx)
+        const float2* src = A.ws + (int64_t)(w % A.S) * MQD + (int64_t)h16 * (Q * D) + idx * 16 + (c16 & 3) * 4 +
+                            (c16 >> 2);
+#pragma unroll
+        for (int k = 0; k < R1; ++k) pre[k] = ld_cg(src + (int64_t)(16 * k) * (Q * D));
+    };
+    auto load_first = [&](int isA, int w, int idx) {   // first tile of a job
+        if (isA) {
+            if (tid < 16 * AC) load_f(w, idx * AC);
+            else load_g(idx * AC, 0, 0);   // idle in the Zak DFT: fetch u-tile 0's G' now
+        } else {
+            load_ring(w, idx * BT);
+        }
+    };
+    int pnext = -1;
+    // Cross-job prefetch.  claim_ready (thread 0, before the last tile's exchange barrier)
+    // publishes the next job and whether its inputs may be read now (A: always -- f and G'
+    // are read-only; B: its dependency already holds).  prefetch_next (every thread, after
+    // that barrier, when pre[] is dead) loads them behind the tile's stage 2.
+    auto claim_ready = [&]() {
+        int isA0, idx0, w0, ready = 0;
+        if (decode(pnext, A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
+            const int gen0 = w0 / A.S, slot0 = w0 - gen0 * A.S;
+            ready = isA0 || (A.dbg & 1) || ld_acquire(doneA + slot0) >= (gen0 + 1) * A.nA;
+        }
+        jobsm[0] = pnext;
+        jobsm[1] = ready;
+    };
+    auto prefetch_next = [&]() {
+        int isA0, idx0, w0;
+        if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) load_first(isA0, w0, idx0);
+    };
+    // ---- dynamic job queue: thread 0 claims the next job at the start of the current
+    // job's last tile (the atomic's latency overlaps that tile) and spins on its dependency
+    // at the top of the next iteration ----
+    if (tid == 0) {
+        jobsm[0] = atomicAdd(queue, 1);
+        jobsm[1] = 0;
+    }
+    __syncthreads();
+    for (;;) {
+        const int p = jobsm[0];
+        const int pref = jobsm[1];
+        int isA, idx, w;
+        if (!decode(p, A.W, A.lag, A.nA, A.nB, &isA, &w, &idx)) break;
+        const int gen = w / A.S, slot = w - gen * A.S;
+        float2* wsl = A.ws + (int64_t)slot * MQD;
+        mark(isA ? 1 : 2);
+        __syncthreads();   // everyone has read jobsm; the previous job is done with X/F
+        mark(3);
+        if (tid == 0 && !(A.dbg & 1)) {
+            if (isA) spin_until(doneB + slot, gen * A.nB);                 // slot free: B(w - S) done
+            else if (!pref) spin_until(doneA + slot, (gen + 1) * A.nA);   // all A(w) done
+        }
+        // B inputs may be read only after the spin.  (A jobs: thread 0's spin precedes its
+        // first exchange barrier, hence every ring store.)
+        mark(4);
+        if (!pref) {
+            if (!isA) __syncthreads();
+            load_first(isA, w, idx);
+        }
+        mark(pref ? 6 : 5);
+        auto none = [] {};
+        if (isA) {
+            // ---------------- pass A: columns j0 .. j0 + 7 ----------------
+            const int j0 = idx * AC;
+            if (tid < 16 * AC) {   // warps 0-3: the Zak DFT of 8 columns
+                // F_j(nu), nu = 16 r + i + R1 m2
+                dft_tile<D>(pre, twt + h8 * 16, X2, c8, h8, c8, h8, none, [&] { load_g(j0, 0, 0); },
+                            [&](int r, const float2* y) {
+#pragma unroll
+                                for (int m2 = 0; m2 < 16; ++m2) {
+                                    const int nu = 16 * r + h8 + R1 * m2;
+                                    F[c8 * D + (nu ^ (2 * c8))] = y[m2];
+                                }
+                            }, A.dbg, mark);
+            } else {
+                dft_tile_idle();
+            }
+            mark(20);
+            __syncthreads();
+            mark(21);
+            // two tiles of 16 slots: tile h = columns j0 + 4h .. + 3, slot s -> (col = s >> 2, u = s & 3)
+            const int wq = tid >> 5, ln = tid & 31;
+            const int colM = wq >> 1, uM = ln >> 3, iM = (ln & 7) + 8 * (wq & 1);   // role M3
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int fcol = 4 * h + (c16 >> 2);   // F column of this S1 slot
+                const int jS = j0 + fcol;
+                const int sig = (int)((((int64_t)jS * A.beta - ((int64_t)A.Kmod * jS) % D) % D + D) % D);
+                if (h == 1 && tid == 0) pnext = atomicAdd(queue, 1);
+                // x(t + 16k) = F((sigma - t - 16k) mod D) G'(t + 16k); G' values k < 16 were
+                // prefetched behind the previous tile, the rest are loaded now
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int e = (sig - h16 - 16 * k) & (D - 1);
+                    pre[k] = cmw(F[fcol * D + (e ^ (2 * fcol))], pre[k]);
+                }
+                if (R1 > 16) {
+                    asm volatile("" ::: "memory");
+                    load_g(j0, h, 1);
+#pragma unroll
+                    for (int k = 16; k < R1; ++k) {
+                        const int e = (sig - h16 - 16 * k) & (D - 1);
+                        pre[k] = cmw(F[fcol * D + (e ^ (2 * fcol))], pre[k]);
+                    }
+                }
+                mark(22);
+                if (h) __syncthreads();   // previous tile's readers are done with X
+                // ring layout ws[slot][j][n' >> 2][kappa][n' & 3]: one 128-byte line per
+                // (j, n' >> 2) = exactly the line one B job reads.  A warp of role M3 holds the
+                // 4 kappa of one column x 8 consecutive n': every store fills 2 whole lines.
+                const int jM = j0 + 4 * h + colM;
+                const int kap = ((jM / A.c - uM) % Q + Q) % Q;
+                float2* dst = wsl + (int64_t)jM * (Q * D) + kap * 4;
+                dft_tile<D>(pre, twt + h16 * 16, X2, c16, h16, 4 * colM + uM, iM,
+                            [&] { if (h == 1 && tid == 0) claim_ready(); },
+                            [&] { if (h == 0) load_g(j0, 1, 0); else prefetch_next(); },
+                            [&](int r, const float2* y) {
+                                if (A.dbg & 4) return;
+#pragma unroll
+                                for (int m2 = 0; m2 < 16; ++m2) {
+                                    const int np = 16 * r + iM + R1 * m2;
+                                    dst[(np >> 2) * 16 + (np & 3)] = y[m2];
+                                }
+                            }, A.dbg, mark);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(doneA + slot, 1);
+            }
+        } else {
+            // ---------------- pass B: columns 16 BT idx .. + 16 BT (BT tiles) ----------------
+#pragma unroll 1
+            for (int bt = 0; bt < BT; ++bt) {
+                const int line = idx * BT + bt;   // ring line (j, line) = columns 16 line .. + 16
+                if (bt == BT - 1 && tid == 0) pnext = atomicAdd(queue, 1);
+                const int n = line * 16 + c16;
+                const float2 e = __ldg(A.E + n);
+                float2* dst = A.out + (int64_t)w * M * A.N + n;
+                if (bt) __syncthreads();   // previous tile's readers are done with X
+                dft_tile<D>(pre, twt + h16 * 16, X2, c16, h16, c16, h16,
+                            [&] { if (bt == BT - 1 && tid == 0) claim_ready(); },
+                            [&] { if (bt + 1 < BT) load_ring(w, line + 1); else prefetch_next(); },
+                            [&](int r, const float2* y) {
+                                if (A.dbg & 4) return;
+#pragma unroll
+                                for (int m2 = 0; m2 < 16; ++m2) {
+                                    const int m = 16 * r + h16 + R1 * m2;
+                                    __stcs(dst + (int64_t)m * A.N, cmw(y[m2], e));
+                                }
+                            }, A.dbg, mark);
+                // The ring lines this tile read are dead (this job is their only reader; the
+                // exchange barrier inside dft_tile ordered every load before this point):
+                // drop them from L2 so they are never written back to HBM.  Half-warp t
+                // owns lines j = t + 16 k; lane col drops k = col (+ 16).
+#pragma unroll
+                for (int k = c16; k < R1; k += 16)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(wsl + (int64_t)(h16 + 16 * k) * (Q * D) + line * 16)
+                                 : "memory");
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(doneB + slot, 1);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// plan-time table G' (fp64 arithmetic, stored once as complex64)
+// ------------------------------------------------------------------------------------
+struct GpArgs {
+    float4* Gp;            // [M][Q][R1/2][16] float4
+    const double2* G64;    // [(r*Q + u)*D + nu] = conj(Gamma_r(u; nu))/d
+    int64_t L, K;          // chirp exponent K = sigma (L+1) mod 2L
+    int M, D, Q, c, beta, R1;
+    int alpha[16];         // alpha_{l,u}, l,u < Q
+};
+
+__global__ void k_gprime(GpArgs a) {
+    const int64_t total = (int64_t)a.M * a.Q * a.D;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int mu = (int)(i % a.D);
+        const int u = (int)((i / a.D) % a.Q);
+        const int j = (int)(i / ((int64_t)a.D * a.Q));
+        const int r = j % a.c, l = j / a.c;
+        const int e = (l >= u) ? 0 : -1;   // floor((l - u)/q) for l, u < q
+        const int gi = (int)((((int64_t)j * a.beta - mu) % a.D + a.D) % a.D);
+        const double2 g = a.G64[((int64_t)r * a.Q + u) * a.D + gi];
+        // C(j) = exp(i pi (K j^2 mod 2L) / L)
+        const unsigned __int128 twoL = 2 * (unsigned __int128)a.L;
+        const unsigned __int128 ce = ((unsigned __int128)a.K * (((unsigned __int128)j * j) % twoL)) % twoL;
+        double s1, c1;
+        sincospi((double)(int64_t)ce / (double)a.L, &s1, &c1);
+        // W_D^{j alpha - mu e}
+        const int64_t ex = (((int64_t)j * a.alpha[l * a.Q + u] - (int64_t)mu * e) % a.D + a.D) % a.D;
+        double s2, c2;
+        sincospi(-2.0 * (double)ex / (double)a.D, &s2, &c2);
+        const double pr = c1 * c2 - s1 * s2, pi = c1 * s2 + s1 * c2;
+        const double vr = g.x * pr - g.y * pi, vi = g.x * pi + g.y * pr;
+        // layout [j / 8][h][kp][t][slot][2]: j = 8 jb + 4 h + col, slot = 4 col + u, mu = t + 16 k,
+        // k = 2 kp + hh (the order one u-tile of fused7_kernel reads it)
+        const int t = mu & 15, k = mu >> 4;
+        const int jb = j / 8, hq = (j % 8) / 4, col = j % 4, sl = 4 * col + u;
+        float2* dst = reinterpret_cast<float2*>(a.Gp) +
+                      (((((int64_t)jb * 2 + hq) * (a.R1 / 2) + (k >> 1)) * 16 + t) * 16 + sl) * 2 + (k & 1);
+        *dst = make_float2((float)vr, (float)vi);
+    }
+}
+
+}  // namespace v7
+}  // namespace nsdgt
