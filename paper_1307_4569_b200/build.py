@@ -34,6 +34,8 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    if os.environ.get("NSDGT_TRACE"):
+        NVCC_FLAGS.append("-DNSDGT_TRACE")
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"

@@ -689,7 +689,7 @@ int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, cons
     if constexpr (!std::is_same<T, float>::value) return DGT_OK;
     if (std::getenv("NSDGT_V6")) return DGT_OK;
     if (I.branch == DGT_BRANCH_FREQ || I.p != 1 || I.q != 4 || I.d != I.iM || (I.d != 512 && I.d != 256)) return DGT_OK;
-    if (I.c % 16 != 0 || I.N % (16 * v7::Cfg<512>::BT) != 0 || I.iM != I.M) return DGT_OK;
+    if (I.c % 16 != 0 || I.N % (16 * v7::Cfg<512>::BT) != 0 || I.iM != I.M || I.N != I.q * I.d) return DGT_OK;
     const int64_t L = I.L, twoL = 2 * L, D = I.d, M = I.M, Q = I.q, N = I.N;
     const int64_t sigma = ((I.chirp_sigma % twoL) + twoL) % twoL;
     const int64_t K = (int64_t)((unsigned __int128)sigma * (unsigned __int128)((L + 1) % twoL) % (unsigned __int128)twoL);

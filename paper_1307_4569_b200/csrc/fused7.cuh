@@ -287,6 +287,7 @@ template <int D>
 __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
     using K = Cfg<D>;
     constexpr int R1 = K::R1, Q = K::Q, M = D, AC = K::ACOL, BT = K::BT;
+    constexpr int N = Q * D;       // N = L / a = q d here (the host checks)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* X2 = reinterpret_cast<float2*>(smem_raw);
     float2* F = X2 + K::XE;        // F[col][nu ^ 2 col], col < ACOL
@@ -304,11 +305,16 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
         sincospi(-2.0 * (double)((tt * m) % D) / (double)D, &s, &c);
         twt[e] = make_float2((float)c, (float)s);
     }
+#ifdef NSDGT_TRACE
+    // phase trace (tools/v7trace.py): thread 0 of CTAs < 8 logs globaltimer stamps
     unsigned long long* lg = (A.dbg & 16) && blockIdx.x < 8 && tid == 0 ? A.log + (size_t)blockIdx.x * 4096 : nullptr;
     int nlog = 0;
     auto mark = [&](int code) {
         if (lg && nlog < 4095) lg[nlog++] = (gtimer() << 8) | (unsigned long long)code;
     };
+#else
+    auto mark = [](int) {};
+#endif
     int* queue = A.ctr;
     int* doneA = A.ctr + 1;
     int* doneB = A.ctr + 1 + A.S;
@@ -316,10 +322,12 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
 
     // ---- global inputs of a tile, loaded into pre[] (this thread's role) ----
     float2 pre[R1];
-    auto load_f = [&](int w, int j0) {          // Zak DFT input (role S1_8, tid < 128)
+    // values k in [16 b, 16 b + 16) of a tile's inputs -> pre[] (halves keep a cross-tile
+    // prefetch within the register budget)
+    auto load_f = [&](int w, int j0, int b) {   // Zak DFT input (role S1_8, tid < 128)
         const float2* fw = A.f + (int64_t)w * M * D + j0 + c8;
 #pragma unroll
-        for (int k = 0; k < R1; ++k) pre[k] = ld_cs(fw + (int64_t)(h8 + 16 * k) * M);
+        for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ld_cs(fw + (int64_t)(h8 + 16 * k) * M);
     };
     // G' of u-tile h (role S1_16: slot c16 = 4 col + u, lane t): values k in [16 b, 16 b + 16).
     // Layout [j0 / 8][h][kp][t][slot] of float4 (k = 2 kp, 2 kp + 1): a half-warp reads 256
@@ -333,18 +341,18 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
             pre[2 * kp + 1] = make_float2(g.z, g.w);
         }
     };
-    auto load_ring = [&](int w, int idx) {      // pass-B input (role S1_16): line (j, idx)
-        const float2* src = A.ws + (int64_t)(w % A.S) * MQD + (int64_t)h16 * (Q * D) + idx * 16 + (c16 & 3) * 4 +
+    auto load_ring = [&](int w, int line, int b) {   // pass-B input (role S1_16): line (j, line)
+        const float2* src = A.ws + (int64_t)(w % A.S) * MQD + (int64_t)h16 * (Q * D) + line * 16 + (c16 & 3) * 4 +
                             (c16 >> 2);
 #pragma unroll
-        for (int k = 0; k < R1; ++k) pre[k] = ld_cg(src + (int64_t)(16 * k) * (Q * D));
+        for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ld_cg(src + (int64_t)(16 * k) * (Q * D));
     };
-    auto load_first = [&](int isA, int w, int idx) {   // first tile of a job
+    auto load_first = [&](int isA, int w, int idx, int b) {   // first tile of a job, half b
         if (isA) {
-            if (tid < 16 * AC) load_f(w, idx * AC);
-            else load_g(idx * AC, 0, 0);   // idle in the Zak DFT: fetch u-tile 0's G' now
+            if (tid < 16 * AC) load_f(w, idx * AC, b);
+            else load_g(idx * AC, 0, b);   // idle in the Zak DFT: fetch u-tile 0's G' now
         } else {
-            load_ring(w, idx * BT);
+            load_ring(w, idx * BT, b);
         }
     };
     int pnext = -1;
@@ -363,11 +371,23 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
     };
     auto prefetch_next = [&]() {
         int isA0, idx0, w0;
-        if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) load_first(isA0, w0, idx0);
+        if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) load_first(isA0, w0, idx0, 0);
     };
     // ---- dynamic job queue: thread 0 claims the next job at the start of the current
     // job's last tile (the atomic's latency overlaps that tile) and spins on its dependency
     // at the top of the next iteration ----
+    // Completion signals are deferred: thread 0 publishes "job done" (fence + counter add)
+    // once it is into its next job's first tile, when the job's stores have drained and
+    // the fence is cheap -- or before any spin, so it never waits on its own signal.  The
+    // loop-top barrier orders every thread's stores (and L2 discards) before that fence.
+    int* pend = nullptr;
+    auto flush = [&]() {
+        if (pend) {
+            __threadfence();
+            atomicAdd(pend, 1);
+            pend = nullptr;
+        }
+    };
     if (tid == 0) {
         jobsm[0] = atomicAdd(queue, 1);
         jobsm[1] = 0;
@@ -381,19 +401,24 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
         const int gen = w / A.S, slot = w - gen * A.S;
         float2* wsl = A.ws + (int64_t)slot * MQD;
         mark(isA ? 1 : 2);
-        __syncthreads();   // everyone has read jobsm; the previous job is done with X/F
+        __syncthreads();   // everyone has read jobsm; the previous job is done with X/F, its stores are ordered
         mark(3);
         if (tid == 0 && !(A.dbg & 1)) {
-            if (isA) spin_until(doneB + slot, gen * A.nB);                 // slot free: B(w - S) done
-            else if (!pref) spin_until(doneA + slot, (gen + 1) * A.nA);   // all A(w) done
+            const int* cnt = isA ? doneB + slot : (pref ? nullptr : doneA + slot);
+            const int target = isA ? gen * A.nB : (gen + 1) * A.nA;   // A: slot free (B(w - S) done); B: all A(w) done
+            if (cnt && ld_acquire(cnt) < target) {
+                flush();
+                spin_until(cnt, target);
+            }
         }
+        mark(4);
         // B inputs may be read only after the spin.  (A jobs: thread 0's spin precedes its
         // first exchange barrier, hence every ring store.)
-        mark(4);
         if (!pref) {
             if (!isA) __syncthreads();
-            load_first(isA, w, idx);
+            load_first(isA, w, idx, 0);
         }
+        if (R1 > 16) load_first(isA, w, idx, 1);
         mark(pref ? 6 : 5);
         auto none = [] {};
         if (isA) {
@@ -401,7 +426,8 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
             const int j0 = idx * AC;
             if (tid < 16 * AC) {   // warps 0-3: the Zak DFT of 8 columns
                 // F_j(nu), nu = 16 r + i + R1 m2
-                dft_tile<D>(pre, twt + h8 * 16, X2, c8, h8, c8, h8, none, [&] { load_g(j0, 0, 0); },
+                dft_tile<D>(pre, twt + h8 * 16, X2, c8, h8, c8, h8, [&] { if (tid == 0) flush(); },
+                            [&] { load_g(j0, 0, 0); },
                             [&](int r, const float2* y) {
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) {
@@ -460,11 +486,7 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
                                 }
                             }, A.dbg, mark);
             }
-            __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                atomicAdd(doneA + slot, 1);
-            }
+            if (tid == 0) pend = doneA + slot;
         } else {
             // ---------------- pass B: columns 16 BT idx .. + 16 BT (BT tiles) ----------------
 #pragma unroll 1
@@ -473,17 +495,25 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
                 if (bt == BT - 1 && tid == 0) pnext = atomicAdd(queue, 1);
                 const int n = line * 16 + c16;
                 const float2 e = __ldg(A.E + n);
-                float2* dst = A.out + (int64_t)w * M * A.N + n;
+                float2* dst = A.out + (int64_t)w * M * N + n;
                 if (bt) __syncthreads();   // previous tile's readers are done with X
                 dft_tile<D>(pre, twt + h16 * 16, X2, c16, h16, c16, h16,
-                            [&] { if (bt == BT - 1 && tid == 0) claim_ready(); },
-                            [&] { if (bt + 1 < BT) load_ring(w, line + 1); else prefetch_next(); },
+                            [&] {
+                                if (tid == 0) {
+                                    flush();
+                                    if (bt == BT - 1) claim_ready();
+                                }
+                            },
+                            [&] {
+                                if (bt + 1 < BT) load_ring(w, line + 1, 0), load_ring(w, line + 1, 1);
+                                else prefetch_next();
+                            },
                             [&](int r, const float2* y) {
                                 if (A.dbg & 4) return;
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) {
                                     const int m = 16 * r + h16 + R1 * m2;
-                                    __stcs(dst + (int64_t)m * A.N, cmw(y[m2], e));
+                                    __stcs(dst + m * N, cmw(y[m2], e));
                                 }
                             }, A.dbg, mark);
                 // The ring lines this tile read are dead (this job is their only reader; the
@@ -495,13 +525,11 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
                     asm volatile("discard.global.L2 [%0], 128;" ::"l"(wsl + (int64_t)(h16 + 16 * k) * (Q * D) + line * 16)
                                  : "memory");
             }
-            __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                atomicAdd(doneB + slot, 1);
-            }
+            if (tid == 0) pend = doneB + slot;
         }
     }
+    __syncthreads();   // the last job's stores are ordered before its completion signal
+    if (tid == 0) flush();
 }
 
 // ------------------------------------------------------------------------------------
