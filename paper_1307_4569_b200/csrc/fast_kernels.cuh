@@ -527,7 +527,7 @@ struct FastPlan {
     bool persist = false;   // L2 persisting window over the intermediate workspace
     // kind 2 (fused7): per-column window table G', ring of S7 slots, look-ahead lag7
     void* Gp7 = nullptr;
-    int beta7 = 0, S7 = 6, lag7 = 4;
+    int beta7 = 0, S7 = 8, lag7 = 5, minb7 = 3;
 };
 
 template <typename T, int D, int MM, int Q, int NCOL>
@@ -661,7 +661,7 @@ inline size_t fast_workspace_bytes(const FastPlan* fp, int64_t /*Wc*/) {
 inline int64_t fast_chunk(const FastPlan*) { return (int64_t)1 << 40; }
 inline int64_t fast_launches_per_chunk(const FastPlan*) { return 1; }
 
-template <int D>
+template <int D, int MINB>
 static void launch7(const v7::Args& a, int grid, size_t smem, cudaStream_t st, const cudaAccessPolicyWindow* apw) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -678,7 +678,7 @@ static void launch7(const v7::Args& a, int grid, size_t smem, cudaStream_t st, c
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, v7::fused7_kernel<D>, a);
+    cudaLaunchKernelEx(&cfg, v7::fused7_kernel<D, MINB>, a);
 }
 
 // kind 2: the fused7 kernel (fused7.cuh).  Builds G' from the fp64 window factors and checks,
@@ -689,7 +689,7 @@ int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, cons
     if constexpr (!std::is_same<T, float>::value) return DGT_OK;
     if (std::getenv("NSDGT_V6")) return DGT_OK;
     if (I.branch == DGT_BRANCH_FREQ || I.p != 1 || I.q != 4 || I.d != I.iM || (I.d != 512 && I.d != 256)) return DGT_OK;
-    if (I.c % 16 != 0 || I.N % (16 * v7::Cfg<512>::BT) != 0 || I.iM != I.M || I.N != I.q * I.d) return DGT_OK;
+    if (I.c % 16 != 0 || I.N % 16 != 0 || I.iM != I.M || I.N != I.q * I.d) return DGT_OK;
     const int64_t L = I.L, twoL = 2 * L, D = I.d, M = I.M, Q = I.q, N = I.N;
     const int64_t sigma = ((I.chirp_sigma % twoL) + twoL) % twoL;
     const int64_t K = (int64_t)((unsigned __int128)sigma * (unsigned __int128)((L + 1) % twoL) % (unsigned __int128)twoL);
@@ -724,17 +724,20 @@ int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, cons
     if (cudaStreamSynchronize(st) != cudaSuccess) { cudaFree(G64); return DGT_ECUDA; }
     cudaFree(G64);
     size_t smem = D == 512 ? v7::Cfg<512>::SMEM : v7::Cfg<256>::SMEM;
-    auto kfn = D == 512 ? (const void*)v7::fused7_kernel<512> : (const void*)v7::fused7_kernel<256>;
+    // CTAs per SM: 3 (no register spills) by default; NSDGT_CTAS=4 trades spills for warps
+    fp->minb7 = (std::getenv("NSDGT_CTAS") && std::atoi(std::getenv("NSDGT_CTAS")) == 4) ? 4 : 3;
+    const void* kfn = D == 512 ? (fp->minb7 == 4 ? (const void*)v7::fused7_kernel<512, 4> : (const void*)v7::fused7_kernel<512, 3>)
+                               : (fp->minb7 == 4 ? (const void*)v7::fused7_kernel<256, 4> : (const void*)v7::fused7_kernel<256, 3>);
     if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return DGT_ECUDA;
     int per_sm = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, v7::Cfg<512>::NT, smem) != cudaSuccess || per_sm < 1)
         return DGT_EUNSUPPORTED;
     fp->grid = per_sm * sms;
     fp->smem = smem;
     fp->D = (int)D; fp->MM = (int)M; fp->Q = (int)Q; fp->c = (int)I.c; fp->N = (int)N; fp->L = L;
-    fp->nA = (int)(M / v7::Cfg<512>::ACOL); fp->nB = (int)(N / (16 * v7::Cfg<512>::BT));
+    fp->nA = (int)(M / v7::Cfg<512>::ACOL); fp->nB = (int)(N / 16);
     fp->Kmod = (int)(K % D);
     fp->beta7 = (int)beta;
     if (const char* e = std::getenv("NSDGT_S")) fp->S7 = std::max(1, std::atoi(e));
@@ -742,22 +745,9 @@ int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, cons
     if (fp->lag7 >= fp->S7) fp->lag7 = fp->S7 - 1;
     fp->E = E;
     fp->esz = sizeof(float2);
-    // L2 set-aside for the ring (NSDGT_PERSIST=0 disables): a persisting access-policy window
+    // No persisting-L2 carve-out: consumed ring lines are discarded (fused7.cuh), and a
+    // device-wide set-aside measurably slows the kernel and everything else in the process.
     fp->persist = false;
-    {
-        const char* e = std::getenv("NSDGT_PERSIST");
-        int maxp = 0;
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        const size_t ring = (size_t)fp->S7 * M * Q * D * sizeof(float2);
-        if (!(e && e[0] == '0') && maxp > 0) {
-            size_t cur = 0;
-            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-            const size_t want = std::min<size_t>((size_t)maxp, ring);
-            if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-            fp->persist = true;
-        }
-        cudaGetLastError();
-    }
     fp->kind = 2;
     fp->name = "fused7_t_p1";
     return DGT_OK;
@@ -792,8 +782,8 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
         apw.hitProp = cudaAccessPropertyPersisting;
         apw.missProp = cudaAccessPropertyStreaming;
         const cudaAccessPolicyWindow* pw = fp->persist ? &apw : nullptr;
-        if (fp->D == 512) launch7<512>(a, fp->grid, fp->smem, st, pw);
-        else launch7<256>(a, fp->grid, fp->smem, st, pw);
+        if (fp->D == 512) (fp->minb7 == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st, pw);
+        else (fp->minb7 == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st, pw);
         return DGT_OK;
     }
     if (!fp->counters) {

@@ -19,18 +19,18 @@
 // index reversal, so ws is already rotated: pass B needs only E(n).  (Derivation:
 // DESIGN.md §4.3; every identity is exact, the table is built in fp64.)
 //
-// Execution: one persistent launch, CTAs of 256 threads pull jobs from a global queue.
-//   A job = 8 consecutive columns j of one signal (1 Zak DFT + q product DFTs each),
-//   B job = 16 consecutive columns n (1 DFT over j each).
+// Execution: one persistent launch, CTAs of 128 threads (4 per SM) pull jobs from a global
+// queue.  A job = 8 consecutive columns j of one signal (1 Zak DFT + q product DFTs each),
+// B job = 16 consecutive columns n (1 DFT over j each; one 128-byte ring line per row j).
 // Dependencies (B(w) after all A(w); A(w) after all B(w - S) because it reuses ring slot
 // w mod S) are per-slot monotone counters; every job a CTA waits on was dequeued earlier
 // by a resident CTA, so the spin cannot deadlock.
 //
-// The D-point DFT of a 16-column tile: D = 16 R1, index x = t + 16 k.  Lane (col, t)
-// holds x(t + 16k), k < R1, loaded straight from global memory (16 columns of a row are
-// 128 contiguous bytes); it runs a register DFT-R1 over k and multiplies W_D^{t m1}.  One
-// shared-memory exchange (in rounds of 16 values of m1 to halve the buffer) gives each
-// lane whole sequences over t; a register DFT-16 finishes X(m1 + R1 m2).  All complex
+// The D-point DFT of an 8-slot tile: D = 16 R1, index x = t + 16 k.  Lane (slot, t) holds
+// x(t + 16k), k < R1, loaded straight from global memory (8 columns of a row are 64
+// contiguous bytes); it runs a register DFT-R1 over k and multiplies W_D^{t m1}.  One
+// shared-memory exchange (in rounds of 16 values of m1 to keep the buffer at 16 KB) gives
+// each lane whole sequences over t; a register DFT-16 finishes X(m1 + R1 m2).  All complex
 // arithmetic is packed FP32x2 (FADD2/FFMA2/FMUL2): one instruction per complex add, two
 // per complex multiply.
 #pragma once
@@ -196,6 +196,14 @@ __device__ __forceinline__ void spin_until(const int* p, int target) {
     while (ld_acquire(p) < target) __nanosleep(64);
 }
 __device__ __forceinline__ float2 ld_cs(const float2* p) { return __ldcs(p); }
+// shared-memory 16-byte load the compiler may not hoist out of loops (the twiddle table is
+// loop-invariant; hoisting it costs 32 registers)
+__device__ __forceinline__ float4 lds128_nohoist(const float4* p) {
+    float4 r;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a));
+    return r;
+}
 __device__ __forceinline__ float2 ld_cg(const float2* p) { return __ldcg(p); }
 
 // job p -> (isA, w, idx): blocks g = 0, 1, ...: A(g) jobs (g < W) then B(g - lag) jobs (g >= lag).
@@ -219,59 +227,65 @@ __device__ __forceinline__ bool decode(int p, int W, int lag, int nA, int nB, in
 template <int D>
 struct Cfg {
     static constexpr int R1 = D / 16;            // stage-1 length (32 or 16)
-    static constexpr int NR = R1 / 16;           // stage-2 sequences per lane (2 or 1)
+    static constexpr int NR = R1 / 16;           // exchange rounds = stage-2 sequences per lane (2 or 1)
     static constexpr int Q = 4;
-    static constexpr int NT = 256;               // 16 column slots x 16 lanes
-    static constexpr int ACOL = 8;               // columns j per A job
-    static constexpr int BT = 1;                 // 16-column tiles per B job
-    static constexpr int XE = 16 * D;            // exchange buffer, complex (16 slots x D)
-    static constexpr int FE = ACOL * D;          // F buffer, complex
+    static constexpr int NS = 8;                 // tile slots (columns or (column, u) pairs)
+    static constexpr int NT = 16 * NS;           // 128 threads: 8 slots x 16 lanes
+    static constexpr int ACOL = 8;               // columns j per A job (1 Zak tile + 4 product tiles)
+    static constexpr int BT = 2;                 // 8-column tiles per B job (16 columns = one ring line)
+    static constexpr int XS = 16 * 17 + 2;       // exchange slot stride (rows of 17, 2 mod 16 per slot)
+    static constexpr int XE = NS * XS;           // exchange buffer, complex: one round (~17.5 KB)
+    static constexpr int FS = D + 2;             // F column stride
+    static constexpr int FE = ACOL * FS;         // F buffer, complex
     static constexpr int TW = 16 * 16;           // twiddle table W_D^{t m}, t, m < 16
     static constexpr size_t SMEM = (size_t)(XE + FE + TW) * 8;
 };
 
-// Exchange buffer, 8-byte slots: slot(col, m1, t) = col*D + m1*16 + (t ^ f(col, m1)),
-// f = (m1 + g(col)) & 15, g(c) = 8 (c & 1) + 2 ((c >> 1) & 3) + (c >> 3) (a permutation of
-// 0..15).  Stage-2 lane i reads sequences m1 = 16 r + i.  Every half-warp access of the
-// thread-role maps below hits 16 distinct bank pairs (tools/bank_check.py).
-template <int D>
-__device__ __forceinline__ int xs(int col, int m1, int t) {
-    const int g = 8 * (col & 1) + 2 * ((col >> 1) & 3) + (col >> 3);
-    return col * D + m1 * 16 + (t ^ ((m1 + g) & 15));
-}
+// Exchange buffer (one round of 16 values m1' = m1 mod 16), 8-byte slots, padded instead of
+// swizzled so that every access is a lane base plus a compile-time offset:
+// slot(s, m1', t) = P(s)*XS + m1'*17 + t, XS = 274 = 2 (mod 16), P(s) = 4 (s & 1) + (s >> 1).
+// Every half-warp access of the thread-role maps below hits 16 distinct bank pairs
+// (tools/bank_check.py).
+__device__ __forceinline__ int xslot(int s) { return (((s & 1) << 2) | (s >> 1)) * (16 * 17 + 2); }
 
-// Stage 1 -> exchange -> stage 2 of a 16-slot D-point DFT tile.
-//   in:  v[k] = x(t + 16 k) of slot s1col, lane t
-//   out: emit(r, y) for r < NR, y[m2] = X(16 r + oi + R1 m2) of slot ocol
-// The writer applies W_D^{t (m1 mod 16)} (table row tw = W_D^{t *}); the reader of
-// sequence m1 = 16 + i applies the rest, W_D^{16 t} = W_32^t (compile-time constants).
-// before_sync() runs after this thread's exchange writes, after_sync() right after the
-// barrier (v is dead by then: the caller may refill its prefetch registers).  Leaves the
-// exchange buffer busy: the caller must __syncthreads before the next write.  Warps that
-// sit a tile out call dft_tile_idle (the same single barrier; warp-uniform branch).
+// Stage 1 -> exchange -> stage 2 of an 8-slot D-point DFT tile (128 threads).
+//   in:  v[k] = x(t + 16 k) of slot s1, lane t
+//   out: emit(r, y) for r < NR, y[m2] = X(16 r + oi + R1 m2) of slot os
+// The writer applies W_D^{t (m1 mod 16)} (table row tw = W_D^{t *}); the reader of round
+// r = 1 applies the rest, W_D^{16 t} = W_32^t (compile-time constants).  Per round: write
+// 16 values, barrier, read one sequence, barrier (the buffer holds one round).  before_sync
+// runs after this thread's first-round writes, after_sync right after the first barrier
+// (v is dead then unless NR = 2 -- the second-round values live in v[16..31]).
 template <int D, class Before, class After, class Emit, class Mark>
-__device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2, int s1col, int t, int ocol, int oi,
+__device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2, int s1, int t, int os, int oi,
                                          Before&& before_sync, After&& after_sync, Emit&& emit, int dbg, Mark&& mark) {
     constexpr int R1 = Cfg<D>::R1, NR = Cfg<D>::NR;
     mark(10);
     if (!(dbg & 8)) dftR<R1>(v);
     mark(11);
-#pragma unroll
-    for (int m = 0; m < R1; ++m) {
-        const float2 val = (m & 15) ? cmw(v[m], tw[m & 15]) : v[m];
-        X2[xs<D>(s1col, m, t)] = val;
-        if ((m & 7) == 7) asm volatile("" ::: "memory");   // bound the twiddle loads in flight
-    }
-    before_sync();
-    mark(12);
-    __syncthreads();
-    mark(13);
-    after_sync();
+    const float4* tw4 = reinterpret_cast<const float4*>(tw);   // twiddle pairs (m, m + 1)
+    float2* xw = X2 + xslot(s1) + t;                           // writer: + 17 m1'
+    const float2* xr = X2 + xslot(os) + 17 * oi;               // reader: + t
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
+#pragma unroll
+        for (int m = 0; m < 16; m += 2) {
+            const float4 w2 = lds128_nohoist(tw4 + (m >> 1));
+            const float2 a = m ? cmw(v[16 * r + m], make_float2(w2.x, w2.y)) : v[16 * r];
+            const float2 b = cmw(v[16 * r + m + 1], make_float2(w2.z, w2.w));
+            xw[17 * m] = a;
+            xw[17 * (m + 1)] = b;
+            if ((m & 7) == 6) asm volatile("" ::: "memory");   // bound the twiddle loads in flight
+        }
+        if (r == 0) before_sync();
+        mark(12);
+        __syncthreads();
+        mark(13);
         float2 y[16];
 #pragma unroll
-        for (int tt = 0; tt < 16; ++tt) y[tt] = X2[xs<D>(ocol, 16 * r + oi, tt)];
+        for (int tt = 0; tt < 16; ++tt) y[tt] = xr[tt];
+        if (r + 1 < NR) __syncthreads();   // round r + 1 reuses the buffer
+        if (r == NR - 1) after_sync();
         if (r == 1) {
 #pragma unroll
             for (int tt = 1; tt < 16; ++tt) y[tt] = cmw(y[tt], w32(tt));
@@ -281,30 +295,30 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
     }
     mark(14);
 }
-__device__ __forceinline__ void dft_tile_idle() { __syncthreads(); }
 
-template <int D>
-__global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
+template <int D, int MINB>
+__global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     using K = Cfg<D>;
     constexpr int R1 = K::R1, Q = K::Q, M = D, AC = K::ACOL, BT = K::BT;
     constexpr int N = Q * D;       // N = L / a = q d here (the host checks)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* X2 = reinterpret_cast<float2*>(smem_raw);
-    float2* F = X2 + K::XE;        // F[col][nu ^ 2 col], col < ACOL
+    float2* F = X2 + K::XE;        // F[col * FS + nu], col < ACOL
     float2* twt = F + K::FE;       // twt[t][m] = W_D^{t m}
     __shared__ int jobsm[2];       // next job, 1 if its first tile's inputs were prefetched
+    __shared__ int jobdec[4];      // decoded current job: isA (or -1 = done), w, idx
     const int tid = threadIdx.x;
-    // thread-role maps (t = stage-1 lane index, i = stage-2 lane index):
-    //   S1_16 / M1_16: slot c16 = tid & 15, t / i = h16 = tid >> 4
-    //   S1_8  / M1_8 : col  c8  = tid & 7,  t / i = h8  = tid >> 3   (tid < 128)
-    //   M3 (u-tiles) : warp w, lane L: slot 4 (w >> 1) + (L >> 3), i = (L & 7) + 8 (w & 1)
-    const int c16 = tid & 15, h16 = tid >> 4, c8 = tid & 7, h8 = (tid >> 3) & 15;
+    // thread-role maps (t = stage-1 lane, i = stage-2 lane):
+    //   S1 / M1 (Zak tile, B tiles, stage 1 of product tiles): slot s8 = tid & 7, t / i = h8 = tid >> 3
+    //   M3 (stage 2 of product tiles): warp w, lane L: slot 4 (w >> 1) + (L >> 3), i = (L & 7) + 8 (w & 1)
+    const int s8 = tid & 7, h8 = tid >> 3;
     for (int e = tid; e < K::TW; e += K::NT) {
         const int tt = e / 16, m = e % 16;
-        double s, c;
-        sincospi(-2.0 * (double)((tt * m) % D) / (double)D, &s, &c);
-        twt[e] = make_float2((float)c, (float)s);
+        double sn, cs;
+        sincospi(-2.0 * (double)((tt * m) % D) / (double)D, &sn, &cs);
+        twt[e] = make_float2((float)cs, (float)sn);
     }
+    const float2* tw = twt + h8 * 16;
 #ifdef NSDGT_TRACE
     // phase trace (tools/v7trace.py): thread 0 of CTAs < 8 logs globaltimer stamps
     unsigned long long* lg = (A.dbg & 16) && blockIdx.x < 8 && tid == 0 ? A.log + (size_t)blockIdx.x * 4096 : nullptr;
@@ -320,46 +334,41 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
     int* doneB = A.ctr + 1 + A.S;
     const int64_t MQD = (int64_t)M * Q * D;
 
-    // ---- global inputs of a tile, loaded into pre[] (this thread's role) ----
+    // ---- global inputs of a tile -> pre[], values k in [16 b, 16 b + 16) (halves keep a
+    // cross-tile prefetch within the register budget) ----
     float2 pre[R1];
-    // values k in [16 b, 16 b + 16) of a tile's inputs -> pre[] (halves keep a cross-tile
-    // prefetch within the register budget)
-    auto load_f = [&](int w, int j0, int b) {   // Zak DFT input (role S1_8, tid < 128)
-        const float2* fw = A.f + (int64_t)w * M * D + j0 + c8;
+    auto load_f = [&](int w, int j0, int b) {   // Zak DFT input: column j0 + s8, rows t + 16 k
+        const float2* fw = A.f + (int64_t)w * M * D + j0 + s8;
 #pragma unroll
         for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ld_cs(fw + (int64_t)(h8 + 16 * k) * M);
     };
-    // G' of u-tile h (role S1_16: slot c16 = 4 col + u, lane t): values k in [16 b, 16 b + 16).
-    // Layout [j0 / 8][h][kp][t][slot] of float4 (k = 2 kp, 2 kp + 1): a half-warp reads 256
-    // contiguous bytes.
+    // G' of product tile h (slot s8 = 4 col + u, lane t).  Layout [j0 / 8][h][kp][t][slot] of
+    // float4 (k = 2 kp, 2 kp + 1): a warp reads 512 contiguous bytes.
     auto load_g = [&](int j0, int h, int b) {
-        const float4* G4 = A.Gp + ((int64_t)((j0 / AC) * 2 + h) * (R1 / 2)) * 256 + h16 * 16 + c16;
+        const float4* G4 = A.Gp + ((int64_t)((j0 / AC) * 4 + h) * (R1 / 2)) * 128 + h8 * 8 + s8;
 #pragma unroll
         for (int kp = 8 * b; kp < 8 * b + 8 && kp < R1 / 2; ++kp) {
-            const float4 g = __ldg(G4 + kp * 256);
+            const float4 g = __ldg(G4 + kp * 128);
             pre[2 * kp] = make_float2(g.x, g.y);
             pre[2 * kp + 1] = make_float2(g.z, g.w);
         }
     };
-    auto load_ring = [&](int w, int line, int b) {   // pass-B input (role S1_16): line (j, line)
-        const float2* src = A.ws + (int64_t)(w % A.S) * MQD + (int64_t)h16 * (Q * D) + line * 16 + (c16 & 3) * 4 +
-                            (c16 >> 2);
+    // pass-B input: ring line (j, line) holds columns n = 16 line + p at position p; tile bt
+    // reads positions 8 bt + s8
+    auto load_ring = [&](int w, int line, int bt, int b) {
+        const float2* src = A.ws + (int64_t)(w % A.S) * MQD + (int64_t)h8 * (Q * D) + line * 16 + 8 * bt + s8;   // (w % S: rare path)
 #pragma unroll
         for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ld_cg(src + (int64_t)(16 * k) * (Q * D));
     };
     auto load_first = [&](int isA, int w, int idx, int b) {   // first tile of a job, half b
-        if (isA) {
-            if (tid < 16 * AC) load_f(w, idx * AC, b);
-            else load_g(idx * AC, 0, b);   // idle in the Zak DFT: fetch u-tile 0's G' now
-        } else {
-            load_ring(w, idx * BT, b);
-        }
+        if (isA) load_f(w, idx * AC, b);
+        else load_ring(w, idx, 0, b);
     };
     int pnext = -1;
     // Cross-job prefetch.  claim_ready (thread 0, before the last tile's exchange barrier)
-    // publishes the next job and whether its inputs may be read now (A: always -- f and G'
-    // are read-only; B: its dependency already holds).  prefetch_next (every thread, after
-    // that barrier, when pre[] is dead) loads them behind the tile's stage 2.
+    // publishes the next job and whether its inputs may be read now (A: always -- f is
+    // read-only; B: its dependency already holds).  prefetch_next (every thread, after that
+    // barrier, when pre[] is dead) loads the first half behind the tile's stage 2.
     auto claim_ready = [&]() {
         int isA0, idx0, w0, ready = 0;
         if (decode(pnext, A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
@@ -373,9 +382,6 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
         int isA0, idx0, w0;
         if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) load_first(isA0, w0, idx0, 0);
     };
-    // ---- dynamic job queue: thread 0 claims the next job at the start of the current
-    // job's last tile (the atomic's latency overlaps that tile) and spins on its dependency
-    // at the top of the next iteration ----
     // Completion signals are deferred: thread 0 publishes "job done" (fence + counter add)
     // once it is into its next job's first tile, when the job's stores have drained and
     // the fence is cheap -- or before any spin, so it never waits on its own signal.  The
@@ -394,15 +400,26 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
     }
     __syncthreads();
     for (;;) {
-        const int p = jobsm[0];
+        // thread 0 decodes the job claimed during the previous job, checks its dependency
+        // (spinning if needed) and broadcasts it with the loop-top barrier, which also
+        // orders the previous job's stores before its deferred completion signal
         const int pref = jobsm[1];
-        int isA, idx, w;
-        if (!decode(p, A.W, A.lag, A.nA, A.nB, &isA, &w, &idx)) break;
+        if (tid == 0) {
+            int isA0, idx0, w0;
+            if (decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
+                jobdec[0] = isA0; jobdec[1] = w0; jobdec[2] = idx0;
+            } else {
+                jobdec[0] = -1;
+            }
+        }
+        mark(1);
+        __syncthreads();
+        mark(3);
+        const int isA = jobdec[0];
+        if (isA < 0) break;
+        const int w = jobdec[1], idx = jobdec[2];
         const int gen = w / A.S, slot = w - gen * A.S;
         float2* wsl = A.ws + (int64_t)slot * MQD;
-        mark(isA ? 1 : 2);
-        __syncthreads();   // everyone has read jobsm; the previous job is done with X/F, its stores are ordered
-        mark(3);
         if (tid == 0 && !(A.dbg & 1)) {
             const int* cnt = isA ? doneB + slot : (pref ? nullptr : doneA + slot);
             const int target = isA ? gen * A.nB : (gen + 1) * A.nA;   // A: slot free (B(w - S) done); B: all A(w) done
@@ -420,84 +437,76 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
         }
         if (R1 > 16) load_first(isA, w, idx, 1);
         mark(pref ? 6 : 5);
-        auto none = [] {};
         if (isA) {
             // ---------------- pass A: columns j0 .. j0 + 7 ----------------
             const int j0 = idx * AC;
-            if (tid < 16 * AC) {   // warps 0-3: the Zak DFT of 8 columns
-                // F_j(nu), nu = 16 r + i + R1 m2
-                dft_tile<D>(pre, twt + h8 * 16, X2, c8, h8, c8, h8, [&] { if (tid == 0) flush(); },
-                            [&] { load_g(j0, 0, 0); },
-                            [&](int r, const float2* y) {
+            // Zak DFT of 8 columns: F_j(nu), nu = 16 r + i + R1 m2, stored at F[col * FS + nu]
+            dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, [&] { if (tid == 0) flush(); }, [&] { load_g(j0, 0, 0); },
+                        [&](int r, const float2* y) {
 #pragma unroll
-                                for (int m2 = 0; m2 < 16; ++m2) {
-                                    const int nu = 16 * r + h8 + R1 * m2;
-                                    F[c8 * D + (nu ^ (2 * c8))] = y[m2];
-                                }
-                            }, A.dbg, mark);
-            } else {
-                dft_tile_idle();
-            }
+                            for (int m2 = 0; m2 < 16; ++m2) {
+                                F[s8 * K::FS + 16 * r + h8 + R1 * m2] = y[m2];
+                            }
+                        }, A.dbg, mark);
             mark(20);
-            __syncthreads();
+            __syncthreads();   // F complete; X free
             mark(21);
-            // two tiles of 16 slots: tile h = columns j0 + 4h .. + 3, slot s -> (col = s >> 2, u = s & 3)
+            // four product tiles: tile h = columns j0 + 2h, j0 + 2h + 1, slot s -> (col = s >> 2, u = s & 3)
             const int wq = tid >> 5, ln = tid & 31;
             const int colM = wq >> 1, uM = ln >> 3, iM = (ln & 7) + 8 * (wq & 1);   // role M3
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                const int fcol = 4 * h + (c16 >> 2);   // F column of this S1 slot
+            for (int h = 0; h < 4; ++h) {
+                const int fcol = 2 * h + (s8 >> 2);   // F column of this stage-1 slot
                 const int jS = j0 + fcol;
                 const int sig = (int)((((int64_t)jS * A.beta - ((int64_t)A.Kmod * jS) % D) % D + D) % D);
-                if (h == 1 && tid == 0) pnext = atomicAdd(queue, 1);
+                if (h == 3 && tid == 0) pnext = atomicAdd(queue, 1);
                 // x(t + 16k) = F((sigma - t - 16k) mod D) G'(t + 16k); G' values k < 16 were
                 // prefetched behind the previous tile, the rest are loaded now
+                // F index (sigma - t - 16 k) mod D = (e0 - 16 k) mod D, e0 = (sigma - t) mod D: the
+                // first (e0 >> 4) + 1 values need no wrap
+                const float2* Fc = F + fcol * K::FS;
+                const int e0 = (sig - h8) & (D - 1);
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const int e = (sig - h16 - 16 * k) & (D - 1);
-                    pre[k] = cmw(F[fcol * D + (e ^ (2 * fcol))], pre[k]);
-                }
+                for (int k = 0; k < 16; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
                 if (R1 > 16) {
                     asm volatile("" ::: "memory");
                     load_g(j0, h, 1);
 #pragma unroll
-                    for (int k = 16; k < R1; ++k) {
-                        const int e = (sig - h16 - 16 * k) & (D - 1);
-                        pre[k] = cmw(F[fcol * D + (e ^ (2 * fcol))], pre[k]);
-                    }
+                    for (int k = 16; k < R1; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
                 }
                 mark(22);
-                if (h) __syncthreads();   // previous tile's readers are done with X
-                // ring layout ws[slot][j][n' >> 2][kappa][n' & 3]: one 128-byte line per
-                // (j, n' >> 2) = exactly the line one B job reads.  A warp of role M3 holds the
-                // 4 kappa of one column x 8 consecutive n': every store fills 2 whole lines.
-                const int jM = j0 + 4 * h + colM;
+                __syncthreads();   // previous tile's readers are done with X
+                // ring layout ws[slot][j][n' >> 2][n' & 3][kappa]: one 128-byte line per
+                // (j, n' >> 2), holding columns n = 4 n' + kappa in natural order.  A warp of
+                // role M3 holds the 4 kappa of one column x 8 consecutive n': every store
+                // fills 2 whole lines.
+                const int jM = j0 + 2 * h + colM;
                 const int kap = ((jM / A.c - uM) % Q + Q) % Q;
-                float2* dst = wsl + (int64_t)jM * (Q * D) + kap * 4;
-                dft_tile<D>(pre, twt + h16 * 16, X2, c16, h16, 4 * colM + uM, iM,
-                            [&] { if (h == 1 && tid == 0) claim_ready(); },
-                            [&] { if (h == 0) load_g(j0, 1, 0); else prefetch_next(); },
+                // n' = 16 r + iM + R1 m2: line n' >> 2 = 4 r + (R1 / 4) m2 + (iM >> 2), position 4 (iM & 3) + kappa
+                float2* dst = wsl + (int64_t)jM * (Q * D) + (iM >> 2) * 16 + (iM & 3) * 4 + kap;
+                dft_tile<D>(pre, tw, X2, s8, h8, 4 * colM + uM, iM,
+                            [&] { if (h == 3 && tid == 0) claim_ready(); },
+                            [&] { if (h < 3) load_g(j0, h + 1, 0); else prefetch_next(); },
                             [&](int r, const float2* y) {
                                 if (A.dbg & 4) return;
 #pragma unroll
-                                for (int m2 = 0; m2 < 16; ++m2) {
-                                    const int np = 16 * r + iM + R1 * m2;
-                                    dst[(np >> 2) * 16 + (np & 3)] = y[m2];
-                                }
+                                for (int m2 = 0; m2 < 16; ++m2) dst[(4 * r + (R1 / 4) * m2) * 16] = y[m2];
                             }, A.dbg, mark);
             }
             if (tid == 0) pend = doneA + slot;
         } else {
-            // ---------------- pass B: columns 16 BT idx .. + 16 BT (BT tiles) ----------------
+            // ---------------- pass B: columns 16 idx .. 16 idx + 15 (ring line idx) ----------------
 #pragma unroll 1
             for (int bt = 0; bt < BT; ++bt) {
-                const int line = idx * BT + bt;   // ring line (j, line) = columns 16 line .. + 16
                 if (bt == BT - 1 && tid == 0) pnext = atomicAdd(queue, 1);
-                const int n = line * 16 + c16;
+                const int n = idx * 16 + 8 * bt + s8;
                 const float2 e = __ldg(A.E + n);
                 float2* dst = A.out + (int64_t)w * M * N + n;
-                if (bt) __syncthreads();   // previous tile's readers are done with X
-                dft_tile<D>(pre, twt + h16 * 16, X2, c16, h16, c16, h16,
+                if (bt) {
+                    if (R1 > 16) load_ring(w, idx, bt, 1);   // second half (the first was prefetched)
+                    __syncthreads();   // previous tile's readers are done with X
+                }
+                dft_tile<D>(pre, tw, X2, s8, h8, s8, h8,
                             [&] {
                                 if (tid == 0) {
                                     flush();
@@ -505,26 +514,24 @@ __global__ void __launch_bounds__(256, 2) fused7_kernel(Args A) {
                                 }
                             },
                             [&] {
-                                if (bt + 1 < BT) load_ring(w, line + 1, 0), load_ring(w, line + 1, 1);
+                                if (bt + 1 < BT) load_ring(w, idx, bt + 1, 0);
                                 else prefetch_next();
                             },
                             [&](int r, const float2* y) {
                                 if (A.dbg & 4) return;
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) {
-                                    const int m = 16 * r + h16 + R1 * m2;
+                                    const int m = 16 * r + h8 + R1 * m2;
                                     __stcs(dst + m * N, cmw(y[m2], e));
                                 }
                             }, A.dbg, mark);
-                // The ring lines this tile read are dead (this job is their only reader; the
-                // exchange barrier inside dft_tile ordered every load before this point):
-                // drop them from L2 so they are never written back to HBM.  Half-warp t
-                // owns lines j = t + 16 k; lane col drops k = col (+ 16).
-#pragma unroll
-                for (int k = c16; k < R1; k += 16)
-                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(wsl + (int64_t)(h16 + 16 * k) * (Q * D) + line * 16)
-                                 : "memory");
             }
+            // The ring lines this job read are dead (this job is their only reader; the
+            // exchange barriers ordered every load before this point): drop them from L2 so
+            // they are never written back to HBM.  Thread tid drops lines j = tid, tid + 128, ...
+#pragma unroll
+            for (int j = tid; j < M; j += K::NT)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(wsl + (int64_t)j * (Q * D) + idx * 16) : "memory");
             if (tid == 0) pend = doneB + slot;
         }
     }
@@ -564,12 +571,12 @@ __global__ void k_gprime(GpArgs a) {
         sincospi(-2.0 * (double)ex / (double)a.D, &s2, &c2);
         const double pr = c1 * c2 - s1 * s2, pi = c1 * s2 + s1 * c2;
         const double vr = g.x * pr - g.y * pi, vi = g.x * pi + g.y * pr;
-        // layout [j / 8][h][kp][t][slot][2]: j = 8 jb + 4 h + col, slot = 4 col + u, mu = t + 16 k,
-        // k = 2 kp + hh (the order one u-tile of fused7_kernel reads it)
+        // layout [j / 8][h][kp][t][slot][2]: j = 8 jb + 2 h + col, slot = 4 col + u, mu = t + 16 k,
+        // k = 2 kp + hh (the order one product tile of fused7_kernel reads it)
         const int t = mu & 15, k = mu >> 4;
-        const int jb = j / 8, hq = (j % 8) / 4, col = j % 4, sl = 4 * col + u;
+        const int jb = j / 8, hq = (j % 8) / 2, col = j % 2, sl = 4 * col + u;
         float2* dst = reinterpret_cast<float2*>(a.Gp) +
-                      (((((int64_t)jb * 2 + hq) * (a.R1 / 2) + (k >> 1)) * 16 + t) * 16 + sl) * 2 + (k & 1);
+                      (((((int64_t)jb * 4 + hq) * (a.R1 / 2) + (k >> 1)) * 16 + t) * 8 + sl) * 2 + (k & 1);
         *dst = make_float2((float)vr, (float)vi);
     }
 }
