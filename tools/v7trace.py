@@ -22,7 +22,7 @@ buf = np.zeros(8 * 4096, dtype=np.uint64)
 rc = cudart.cudaMemcpy(ctypes.c_void_p(buf.ctypes.data), ctypes.c_void_p(ptr.value), ctypes.c_size_t(buf.nbytes), 2)
 assert rc == 0, rc
 print("log ptr", hex(ptr.value), "nonzero entries", int((buf != 0).sum()), "lib", nsdgt.nsdgt.LIB_PATH if hasattr(nsdgt, "nsdgt") else "", flush=True)
-names = {1: "top(A)", 2: "top(B)", 3: "after-bar1", 4: "after-spin", 5: "loaded", 6: "prefetched", 10: "tile-start",
+names = {30: "A-prespin", 31: "B-prespin", 32: "B-prefetched", 1: "top", 2: "top(B)", 3: "after-bar1", 4: "after-spin", 5: "loaded", 6: "prefetched", 10: "tile-start",
          11: "stage1-done", 12: "xwritten", 13: "xbarrier", 14: "tile-end", 20: "fwd-done", 21: "F-barrier", 22: "gather-done"}
 tot = {}
 for c in range(8):
