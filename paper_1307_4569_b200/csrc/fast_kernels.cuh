@@ -740,6 +740,16 @@ int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, cons
     fp->nA = (int)(M / v7::Cfg<512>::ACOL); fp->nB = (int)(N / 16);
     fp->Kmod = (int)(K % D);
     fp->beta7 = (int)beta;
+    // Look-ahead: B(w) is queued lag signals after A(w).  An A job spans a few tiles, so
+    // about 3 x (CTAs / jobs per signal) signals of look-ahead hide the A -> B dependency;
+    // the ring (S signals of intermediate) is capped at ~64 MB so it stays mostly in L2.
+    {
+        const int jps = fp->nA + fp->nB;
+        const size_t per_sig = (size_t)M * Q * D * sizeof(float2);
+        const int smax = std::max(4, (int)((64ull << 20) / per_sig));
+        fp->lag7 = std::max(2, std::min(smax - 3, (3 * fp->grid + jps / 2) / jps));
+        fp->S7 = std::min(smax, fp->lag7 + 3 + fp->lag7 / 4);
+    }
     if (const char* e = std::getenv("NSDGT_S")) fp->S7 = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("NSDGT_LAG")) fp->lag7 = std::max(0, std::atoi(e));
     if (fp->lag7 >= fp->S7) fp->lag7 = fp->S7 - 1;

@@ -1,22 +1,15 @@
-"""Exhaustive shared-memory bank check of the fused7 exchange-buffer swizzle (tools only).
+"""Exhaustive shared-memory bank check of the fused7 layouts (tools only; mirrors fused7.cuh).
 
-Slot(col, m1, t) = col*D + m1*16 + (t ^ f(col, m1)), 8-byte slots, 16 bank pairs per
-128-byte wavefront.  Writers: stage-1 roles (col, t) write m1 = 0..R1-1.  Readers: stage-2
-roles (col, i) read sequences m1 = 16 r + i (r = 0, 1), every t.  Each half-warp access
-must hit 16 distinct bank pairs (identical addresses broadcast)."""
-import itertools
-
-D, R1 = 512, 32
-roles_w = {
-    'S1_16': lambda tid: (tid & 15, tid >> 4),
-    'S1_8': lambda tid: ((tid & 7, tid >> 3) if tid < 128 else None),
-}
-roles_r = {
-    'M1_16': lambda tid: (tid & 15, tid >> 4),
-    'M1_8': lambda tid: ((tid & 7, tid >> 3) if tid < 128 else None),
-    # u-tile stage 2: warp w -> column w >> 1; lane L -> u = L >> 3, i = (L & 7) + 8 (w & 1)
-    'M3': lambda tid: (4 * ((tid >> 5) >> 1) + ((tid & 31) >> 3), ((tid & 31) & 7) + 8 * ((tid >> 5) & 1)),
-}
+8-byte elements, 16 bank pairs per 128-byte wavefront; each half-warp access must hit
+distinct bank pairs (identical addresses broadcast).  Thread-role maps (128 threads):
+  S1 / M1 : slot s8 = tid & 7, t (or i) = tid >> 3
+  M3      : warp w, lane L: slot 4 (w >> 1) + (L >> 3), i = (L & 7) + 8 (w & 1)
+Exchange: slot(s, m1, t) = P(s) XS + 17 m1 + t, P(s) = 4 (s & 1) + (s >> 1), XS = 17*16 + 2
+(one round of 16 m1 values).  Writers (S1) write every m1 < 16 at their t; readers (M1, M3)
+read their sequence m1 = i at every t.  F buffer: column stride D + 2; the Zak tile writes
+F[s8][16 r + i + R1 m2] (M1), product tile h gathers F[2h + (s8 >> 2)][(sigma - t - 16 k) mod D]
+(S1) for sigma = 0.
+"""
 
 
 def wavefronts(addrs):
@@ -26,38 +19,48 @@ def wavefronts(addrs):
     return max(len(v) for v in banks.values())
 
 
-def cost(f):
-    slot = lambda col, m, t: col * D + m * 16 + (t ^ f(col, m))
-    tot = worst = 0
-    for rn, role in roles_w.items():
-        for m in range(R1):
-            for hw in range(16):
-                a = [slot(*((role(hw * 16 + L)[0], m, role(hw * 16 + L)[1]))) for L in range(16) if role(hw * 16 + L)]
-                if a:
-                    w = wavefronts(a); tot += w; worst = max(worst, w)
-    for rn, role in roles_r.items():
-        for r in range(R1 // 16):
-            for tt in range(16):
-                for hw in range(16):
-                    a = []
-                    for L in range(16):
-                        x = role(hw * 16 + L)
-                        if x:
-                            a.append(slot(x[0], 16 * r + x[1], tt))
-                    if a:
-                        w = wavefronts(a); tot += w; worst = max(worst, w)
-    return tot, worst
+S1 = lambda tid: (tid & 7, tid >> 3)
+M1 = S1
+M3 = lambda tid: (4 * ((tid >> 5) >> 1) + ((tid & 31) >> 3), ((tid & 31) & 7) + 8 * ((tid >> 5) & 1))
+XS = 17 * 16 + 2
+P = lambda s: 4 * (s & 1) + (s >> 1)
+xslot = lambda s, m, t: P(s) * XS + 17 * m + t
 
 
-if __name__ == '__main__':
-    cur = lambda c, m: (2 * c + (c >> 3) + m) & 15
-    print('current f = (2c + (c>>3) + m) & 15:', cost(cur))
-    best = None
-    for a, b, e, g in itertools.product(range(16), (1, 3, 5, 7), range(16), range(4)):
-        f = lambda c, m, a=a, b=b, e=e, g=g: (a * c + b * m + e * (c >> 3) + g * (c >> 2)) & 15
-        r = cost(f)
-        if best is None or r < best[0]:
-            best = (r, a, b, e, g)
-            if r[1] == 1:
-                break
-    print('best (total, worst), f = (a c + b m + e (c>>3) + g (c>>2)) & 15:', best)
+def check(D):
+    R1 = D // 16
+    worst = {}
+    hws = [list(range(hw * 16, hw * 16 + 16)) for hw in range(8)]
+    w = 0
+    for m in range(16):
+        for hw in hws:
+            w = max(w, wavefronts([xslot(S1(t)[0], m, S1(t)[1]) for t in hw]))
+    worst["exchange write (S1)"] = w
+    for name, role in (("exchange read (M1)", M1), ("exchange read (M3)", M3)):
+        w = 0
+        for tt in range(16):
+            for hw in hws:
+                w = max(w, wavefronts([xslot(role(t)[0], role(t)[1], tt) for t in hw]))
+        worst[name] = w
+    FS = D + 2
+    w = 0
+    for r in range(R1 // 16):
+        for m2 in range(16):
+            for hw in hws:
+                w = max(w, wavefronts([(t & 7) * FS + 16 * r + (t >> 3) + R1 * m2 for t in hw]))
+    worst["F write (M1)"] = w
+    w = 0
+    for h in range(4):
+        for k in range(R1):
+            for hw in hws:
+                w = max(w, wavefronts([(2 * h + ((t & 7) >> 2)) * FS + ((-(t >> 3) - 16 * k) % D) for t in hw]))
+    worst["F gather (S1)"] = w
+    return worst
+
+
+if __name__ == "__main__":
+    for D in (256, 512):
+        res = check(D)
+        print(f"D={D}:", res)
+        assert max(res.values()) == 1, "bank conflict"
+    print("all half-warp accesses conflict-free")
