@@ -234,10 +234,12 @@ struct Cfg {
     static constexpr int ACOL = 8;               // columns j per A job (1 Zak tile + 4 product tiles)
     static constexpr int BT = 2;                 // 8-column tiles per B job (16 columns = one ring line)
     static constexpr int XS = 16 * 17 + 2;       // exchange slot stride (rows of 17, 2 mod 16 per slot)
-    static constexpr int XE = NS * XS;           // exchange buffer, complex: one round (~17.5 KB)
+    static constexpr int XR = NS * XS;           // one exchange round, complex (~17.5 KB)
+    static constexpr int XE = XR;                // exchange buffer: one round (rounds take turns)
     static constexpr int FS = D + 2;             // F column stride
     static constexpr int FE = ACOL * FS;         // F buffer, complex
-    static constexpr int TW = 16 * 16;           // twiddle table W_D^{t m}, t, m < 16
+    static constexpr int TWS = 18;               // twiddle-table row stride (rows 144 B apart: no bank overlap)
+    static constexpr int TW = 16 * TWS;          // twiddle table W_D^{t m}, t, m < 16
     static constexpr size_t SMEM = (size_t)(XE + FE + TW) * 8;
 };
 
@@ -248,7 +250,9 @@ struct Cfg {
 // (tools/bank_check.py).
 __device__ __forceinline__ int xslot(int s) { return (((s & 1) << 2) | (s >> 1)) * (16 * 17 + 2); }
 
-// Stage 1 -> exchange -> stage 2 of an 8-slot D-point DFT tile (128 threads).
+// Stage 1 -> exchange -> stage 2 of an 8-slot D-point DFT tile (128 threads).  The rounds
+// share one buffer (a double-buffered variant, 35 KB, measured slower: 3 CTAs x 70 KB leave
+// too little L1); the caller puts a barrier between tiles.
 //   in:  v[k] = x(t + 16 k) of slot s1, lane t
 //   out: emit(r, y) for r < NR, y[m2] = X(16 r + oi + R1 m2) of slot os
 // The writer applies W_D^{t (m1 mod 16)} (table row tw = W_D^{t *}); the reader of round
@@ -264,8 +268,8 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
     if (!(dbg & 8)) dftR<R1>(v);
     mark(11);
     const float4* tw4 = reinterpret_cast<const float4*>(tw);   // twiddle pairs (m, m + 1)
-    float2* xw = X2 + xslot(s1) + t;                           // writer: + 17 m1'
-    const float2* xr = X2 + xslot(os) + 17 * oi;               // reader: + t
+    float2* xw = X2 + xslot(s1) + t;                           // writer: + 17 m1' (+ round buffer)
+    const float2* xr = X2 + xslot(os) + 17 * oi;               // reader: + t (+ round buffer)
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
 #pragma unroll
@@ -312,13 +316,13 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     //   S1 / M1 (Zak tile, B tiles, stage 1 of product tiles): slot s8 = tid & 7, t / i = h8 = tid >> 3
     //   M3 (stage 2 of product tiles): warp w, lane L: slot 4 (w >> 1) + (L >> 3), i = (L & 7) + 8 (w & 1)
     const int s8 = tid & 7, h8 = tid >> 3;
-    for (int e = tid; e < K::TW; e += K::NT) {
+    for (int e = tid; e < 16 * 16; e += K::NT) {
         const int tt = e / 16, m = e % 16;
         double sn, cs;
         sincospi(-2.0 * (double)((tt * m) % D) / (double)D, &sn, &cs);
-        twt[e] = make_float2((float)cs, (float)sn);
+        twt[tt * K::TWS + m] = make_float2((float)cs, (float)sn);
     }
-    const float2* tw = twt + h8 * 16;
+    const float2* tw = twt + h8 * K::TWS;
 #ifdef NSDGT_TRACE
     // phase trace (tools/v7trace.py): thread 0 of CTAs < 8 logs globaltimer stamps
     unsigned long long* lg = (A.dbg & 16) && blockIdx.x < 8 && tid == 0 ? A.log + (size_t)blockIdx.x * 4096 : nullptr;
