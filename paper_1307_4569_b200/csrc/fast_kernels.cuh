@@ -734,6 +734,8 @@ int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, cons
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, v7::Cfg<512>::NT, smem) != cudaSuccess || per_sm < 1)
         return DGT_EUNSUPPORTED;
+    // persistent kernel: every CTA must be resident (the occupancy query bounds the grid)
+    if (const char* e = std::getenv("NSDGT_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     fp->grid = per_sm * sms;
     fp->smem = smem;
     fp->D = (int)D; fp->MM = (int)M; fp->Q = (int)Q; fp->c = (int)I.c; fp->N = (int)N; fp->L = L;
