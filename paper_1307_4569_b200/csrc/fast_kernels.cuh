@@ -725,9 +725,15 @@ int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, cons
     cudaFree(G64);
     size_t smem = D == 512 ? v7::Cfg<512>::SMEM : v7::Cfg<256>::SMEM;
     // CTAs per SM: 3 (no register spills) by default; NSDGT_CTAS=4 trades spills for warps
-    fp->minb7 = (std::getenv("NSDGT_CTAS") && std::atoi(std::getenv("NSDGT_CTAS")) == 4) ? 4 : 3;
+    // CTAs per SM (each 128 threads): measured best 3 for D = 512 (more CTAs leave too little
+    // L1 next to 3 x 53 KB of shared memory), 5 for D = 256 (36 KB, 91 registers).  NSDGT_CTAS overrides.
+    fp->minb7 = D == 512 ? 3 : 5;
+    if (const char* e = std::getenv("NSDGT_CTAS")) fp->minb7 = std::max(3, std::min(5, std::atoi(e)));
+    if (D == 512 && fp->minb7 == 5) fp->minb7 = 4;
     const void* kfn = D == 512 ? (fp->minb7 == 4 ? (const void*)v7::fused7_kernel<512, 4> : (const void*)v7::fused7_kernel<512, 3>)
-                               : (fp->minb7 == 4 ? (const void*)v7::fused7_kernel<256, 4> : (const void*)v7::fused7_kernel<256, 3>);
+                               : (fp->minb7 == 5   ? (const void*)v7::fused7_kernel<256, 5>
+                                  : fp->minb7 == 4 ? (const void*)v7::fused7_kernel<256, 4>
+                                                   : (const void*)v7::fused7_kernel<256, 3>);
     if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return DGT_ECUDA;
     int per_sm = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -795,7 +801,7 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
         apw.missProp = cudaAccessPropertyStreaming;
         const cudaAccessPolicyWindow* pw = fp->persist ? &apw : nullptr;
         if (fp->D == 512) (fp->minb7 == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st, pw);
-        else (fp->minb7 == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st, pw);
+        else (fp->minb7 == 5 ? launch7<256, 5> : fp->minb7 == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st, pw);
         return DGT_OK;
     }
     if (!fp->counters) {
