@@ -222,18 +222,25 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
     const C* __restrict__ chirp = (const C*)A.chirp;
     const int64_t Lc = L / c;
 
-    // 1. gather f~(x(r,k,l,s)), x = r + c((k q + p l + s p q) mod (L/c)), rr fastest
-    const int64_t ng = (int64_t)nr * p * d;
-    for (int64_t i = threadIdx.x; i < ng; i += blockDim.x) {
-        const int rr = (int)(i % nr);
-        const int64_t ks = i / nr;  // k*d + s
-        const int64_t s = ks % d, k = ks / d;
-        const int64_t x = r0 + rr + c * ((k * q + p * l + s * p * q) % Lc);
+    // 1. gather f~(x(r,k,l,s)), x = r + c((k q + p l + s p q) mod (L/c)), rr fastest.
+    //    32-bit index arithmetic within a signal (the host checks L < 2^31).
+    const int ng = nr * (int)p * (int)d;
+    const int di = (int)d, pi = (int)p, qi = (int)q, ci = (int)c, Lci = (int)Lc;
+    const int base_kq = pi * l;                     // p l
+    const T* fr = (const T*)A.f + w * L;            // real input
+    const C* fc = (const C*)A.f + w * L;
+    for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+        const int rr = i % nr;
+        const int ks = i / nr;  // k*d + s
+        const int s = ks % di, k = ks / di;
+        int z = k * qi + base_kq + s * pi * qi;     // < p q (d + 1): fits
+        z %= Lci;
+        const int x = (int)r0 + rr + ci * z;
         C v;
-        if (A.real_in) v = mk<T>(((const T*)A.f)[w * L + x], T(0));
-        else v = ((const C*)A.f)[w * L + x];
+        if (A.real_in) v = mk<T>(fr[x], T(0));
+        else v = fc[x];
         if (chirp) v = cmul(v, chirp[x]);
-        bufA[(rr * p + k) * d + s] = v;
+        bufA[(rr * pi + k) * di + s] = v;
     }
     __syncthreads();
     // 2. DFT_d over s for nr*p sequences
@@ -257,14 +264,17 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
         C* Y = fft_smem<T>(free0, bufY, A.rd, nr, (int)d, tw);
         // 5. scatter T_r(l,u;tau) to n = (l - u - q tau) mod N:
         //    kappa = (l-u) mod q, n' = (-tau - [l<u]) mod d, C[w][j'][kappa][n']
-        const int64_t kappa = ((l - u) % q + q) % q;
-        const int64_t off = (l < u) ? 1 : 0;
-        for (int64_t i = threadIdx.x; i < (int64_t)nr * d; i += blockDim.x) {
-            const int rr = (int)(i / d);
-            const int64_t np = i % d;                 // destination n'
-            const int64_t tau = ((-np - off) % d + d) % d;
-            const int64_t j = r0 + rr + c * jp;
-            Cout[((w * A.iM + j) * q + kappa) * d + np] = Y[rr * d + tau];
+        const int kappa = (int)(((l - u) % q + q) % q);
+        const int off = (l < u) ? 1 : 0;
+        C* Cw = Cout + w * A.iM * q * d;
+        const int jbase = (int)(r0 + c * jp);
+        for (int i = threadIdx.x; i < nr * di; i += blockDim.x) {
+            const int rr = i / di;
+            const int np = i - rr * di;                // destination n'
+            int tau = di - np - off;                   // (-n' - off) mod d
+            if (tau >= di) tau -= di;
+            if (tau < 0) tau += di;
+            Cw[((jbase + rr) * qi + kappa) * di + np] = Y[rr * di + tau];
         }
         __syncthreads();
     }
@@ -285,7 +295,30 @@ struct OutArgs {
     // F-branch
     const void* ptab;
     int64_t L, b, Nr, ar, s1, C1, C2, C3, C4, C5, C6;
+    const int* ktab;               // per inner channel k < N_r: [C1 k mod 2N | C5 k mod 2N | (-s1 a_r k) mod L]
+    unsigned long long inv2N, invL;   // Barrett constants floor(2^64 / 2N), floor(2^64 / L)
 };
+
+// x mod m for x < 2^64, 2 <= m < 2^32 (Barrett: inv = floor((2^64 - 1) / m); the quotient
+// estimate is at most 2 short)
+__device__ __forceinline__ unsigned int bmod(unsigned long long x, unsigned int m, unsigned long long inv) {
+    const unsigned long long qe = __umul64hi(x, inv);
+    unsigned long long r = x - qe * m;
+    if (r >= m) r -= m;
+    if (r >= m) r -= m;
+    return (unsigned int)r;
+}
+
+// F-branch per-channel table (plan time, exact integers)
+__global__ void k_fbranch_ktab(int* kt, int64_t Nr, int64_t twoN, int64_t L, int64_t C1, int64_t C5, int64_t s1,
+                               int64_t ar) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < Nr; k += (int64_t)gridDim.x * blockDim.x) {
+        kt[k] = (int)((((unsigned __int128)C1 * k) % twoN));
+        kt[Nr + k] = (int)((((unsigned __int128)C5 * k) % twoN));
+        const __int128 v = -(((__int128)(s1 % L) * (((__int128)ar * k) % L)) % L);
+        kt[2 * Nr + k] = (int)(((v % L) + L) % L);
+    }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
@@ -299,12 +332,14 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
     C* bufA = (C*)smem_raw;
     C* bufB = bufA + (size_t)NT * iM;
     const C* __restrict__ Cin = (const C*)A.C + w * iM * iN;
-    // load columns n0..n0+nt: C(j, n) stored at [j][n mod q][n div q]
-    for (int64_t i = threadIdx.x; i < (int64_t)nt * iM; i += blockDim.x) {
-        const int cl = (int)(i % nt);
-        const int64_t j = i / nt;
-        const int64_t n = n0 + cl;
-        bufA[cl * iM + j] = Cin[(j * q + (n % q)) * d + n / q];
+    const int iMi = (int)iM, qi = (int)q, di = (int)d;
+    // load columns n0..n0+nt: C(j, n) stored at [j][n mod q][n div q] (32-bit indices within a signal)
+    for (int i = threadIdx.x; i < nt * iMi; i += blockDim.x) {
+        const int cl = i % nt;
+        const int j = i / nt;
+        const int n = (int)n0 + cl;
+        const int nq = n / qi;
+        bufA[cl * iMi + j] = Cin[(j * qi + (n - nq * qi)) * di + nq];
     }
     __syncthreads();
     C* X = fft_smem<T>(bufA, bufB, A.rd, nt, (int)iM, (const C*)A.tw);
@@ -312,32 +347,52 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
         // c[w][(m - rot(n)) mod M][n] = E(n) * X(m, n)   (Alg. 1 lines 9-12)
         C* out = (C*)A.out + w * A.M * A.N;
         const C* E = (const C*)A.E;
-        for (int64_t i = threadIdx.x; i < (int64_t)nt * iM; i += blockDim.x) {
-            const int cl = (int)(i % nt);
-            const int64_t mo = i / nt;
-            const int64_t n = n0 + cl;
-            int64_t m = mo + A.rot[n];
-            if (m >= A.M) m -= A.M;
-            out[mo * A.N + n] = cmul(E[n], X[cl * iM + m]);
+        const int Mi = (int)A.M, Ni = (int)A.N;
+        for (int i = threadIdx.x; i < nt * iMi; i += blockDim.x) {
+            const int cl = i % nt;
+            const int mo = i / nt;
+            const int n = (int)n0 + cl;
+            int m = mo + A.rot[n];
+            if (m >= Mi) m -= Mi;
+            out[mo * Ni + n] = cmul(E[n], X[cl * iMi + m]);
         }
     } else {
         // c[kt][mt] = E(k,m) c_r[(-k) mod N_r][m]  (Alg. 1 lines 24-31); here the inner
         // channel is the FFT output index kc = (-k) mod N_r, the inner time index m = n.
+        //   sq = (C1 k + C2 m) mod 2N,  e = (C3 sq^2 - m (C4 m + C5 k)) mod 2N,
+        //   mt = sq mod N,  kt = ((-s1 a_r k + C6 m) mod L) div b
+        // The k-dependent residues come from the plan's per-channel table, the m-dependent
+        // ones are per-column constants; every reduction is exact (Barrett, 64-bit products).
         C* out = (C*)A.out + w * A.M * A.N;
         const C* P = (const C*)A.ptab;
-        const int64_t twoN = 2 * A.N, Nn = A.N, L = A.L;
-        for (int64_t i = threadIdx.x; i < (int64_t)nt * iM; i += blockDim.x) {
-            const int64_t kc = i % iM;
-            const int cl = (int)(i / iM);
-            const int64_t m = n0 + cl;
-            const int64_t k = (A.Nr - kc) % A.Nr;
-            const int64_t sq = (A.C1 * k + A.C2 * (m % twoN)) % twoN;
-            const int64_t t1 = (A.C3 * ((sq * sq) % twoN)) % twoN;
-            const int64_t t2 = ((m % twoN) * ((A.C4 * (m % twoN) + A.C5 * k) % twoN)) % twoN;
-            const int64_t e = ((t1 - t2) % twoN + twoN) % twoN;
-            const int64_t mt = (A.C1 * k + A.C2 * (m % Nn)) % Nn;
-            const int64_t kt = ((((-(A.s1 % L) * ((A.ar * k) % L)) % L + (A.C6 * m) % L) % L + L) % L) / A.b;
-            out[kt * Nn + mt] = cmul(P[e], X[cl * iM + kc]);
+        const unsigned int twoN = (unsigned int)(2 * A.N), Nn = (unsigned int)A.N, Lu = (unsigned int)A.L;
+        const unsigned int bu = (unsigned int)A.b, Nr = (unsigned int)A.Nr;
+        const int* kA = A.ktab;
+        const int* kC = A.ktab + A.Nr;
+        const int* kT = A.ktab + 2 * A.Nr;
+        for (int cl = 0; cl < nt; ++cl) {
+            const unsigned long long m = (unsigned long long)(n0 + cl);
+            const unsigned int mD = bmod(m, twoN, A.inv2N);
+            const unsigned int mA = bmod((unsigned long long)A.C2 * mD, twoN, A.inv2N);
+            const unsigned int mC4 = bmod((unsigned long long)A.C4 * mD, twoN, A.inv2N);
+            const unsigned int mT = bmod((unsigned long long)(A.C6 % A.L) * (m % A.L), Lu, A.invL);
+            const C* Xc = X + cl * iMi;
+            for (int kc = threadIdx.x; kc < iMi; kc += blockDim.x) {
+                const unsigned int k = kc ? Nr - (unsigned int)kc : 0u;
+                unsigned int sq = (unsigned int)kA[k] + mA;
+                if (sq >= twoN) sq -= twoN;
+                const unsigned int s2 = bmod((unsigned long long)sq * sq, twoN, A.inv2N);
+                const unsigned int t1 = bmod((unsigned long long)A.C3 * s2, twoN, A.inv2N);
+                unsigned int uu = mC4 + (unsigned int)kC[k];
+                if (uu >= twoN) uu -= twoN;
+                const unsigned int t2 = bmod((unsigned long long)mD * uu, twoN, A.inv2N);
+                const unsigned int e = t1 >= t2 ? t1 - t2 : t1 + twoN - t2;
+                const unsigned int mt = sq >= Nn ? sq - Nn : sq;
+                unsigned int xx = (unsigned int)kT[k] + mT;
+                if (xx >= Lu) xx -= Lu;
+                const unsigned int kt = xx / bu;
+                out[(size_t)kt * Nn + mt] = cmul(P[e], Xc[kc]);
+            }
         }
     }
 }
@@ -361,6 +416,7 @@ struct Plan {
     void* E = nullptr;       // T-branch column phases (N)
     int* rot = nullptr;      // T-branch rotations (N)
     void* ptab = nullptr;    // F-branch phase table (2N)
+    int* ktab = nullptr;     // F-branch per-channel residues (3 N_r)
     // workspace
     void* Cws = nullptr;     // chunk intermediate
     void* fhat = nullptr;    // F-branch chunk spectra
@@ -423,7 +479,7 @@ static void prof_close(Plan* P, int h, int kind, double bytes, double flops, cud
 
 static void free_plan(Plan* P) {
     if (!P) return;
-    void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
+    void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->ktab, P->Cws, P->fhat,
                     P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1]};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -509,6 +565,9 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
     } else {
         CUDA_TRY(cudaMalloc(&P->ptab, sizeof(C) * 2 * I.N));
         k_phase_table<T><<<grid_for(2 * I.N), 256, 0, st>>>((C*)P->ptab, I.N);
+        CUDA_TRY(cudaMalloc(&P->ktab, sizeof(int) * 3 * I.N_r));
+        k_fbranch_ktab<<<grid_for(I.N_r), 256, 0, st>>>(P->ktab, I.N_r, 2 * I.N, I.L, I.C1 % (2 * I.N), I.C5 % (2 * I.N),
+                                                         I.s1, I.a_r);
     }
     CUDA_TRY(cudaGetLastError());
     int rc = build_fast<T>(&P->fp, P->info, P->G, P->chirp, P->E, P->rot, (P->flags & DGT_FORCE_GENERIC) != 0, st);
@@ -581,7 +640,15 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
     B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
     B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
-    B.C1 = I.C1; B.C2 = I.C2; B.C3 = I.C3; B.C4 = I.C4; B.C5 = I.C5; B.C6 = I.C6;
+    {
+        const int64_t twoN = 2 * I.N;
+        auto nm = [](int64_t v, int64_t m) { return ((v % m) + m) % m; };
+        B.C1 = nm(I.C1, twoN); B.C2 = nm(I.C2, twoN); B.C3 = nm(I.C3, twoN); B.C4 = nm(I.C4, twoN);
+        B.C5 = nm(I.C5, twoN); B.C6 = nm(I.C6, I.L);
+    }
+    B.ktab = P->ktab;
+    B.inv2N = ~0ull / (unsigned long long)(2 * I.N);
+    B.invL = ~0ull / (unsigned long long)I.L;
     const int ntiles = (int)((I.iN + P->NT - 1) / P->NT);
     ph = prof_open(P, st);
     out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
@@ -601,6 +668,9 @@ static int configure(Plan* P, int64_t max_chunk) {
     CUDA_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
     const size_t budget = std::min<size_t>((size_t)smem_optin, 200 * 1024);
     if (I.d > (1 << 30) || I.iM > (1 << 30)) return fail(DGT_EUNSUPPORTED, "inner length too large");
+    // the generic kernels index within one signal in 32-bit arithmetic
+    if (I.L >= ((int64_t)1 << 31) || I.M * I.N >= ((int64_t)1 << 31) || 2 * I.N >= ((int64_t)1 << 31))
+        return fail(DGT_EUNSUPPORTED, "signal too long for 32-bit in-signal indexing");
     P->rd_d = make_radices((int)I.d);
     P->rd_m = make_radices((int)I.iM);
     if (P->rd_d.nst > kMaxStages || P->rd_m.nst > kMaxStages) return fail(DGT_EUNSUPPORTED, "too many FFT stages");
