@@ -238,8 +238,8 @@ struct Cfg {
     static constexpr int XE = XR;                // exchange buffer: one round (rounds take turns)
     static constexpr int FS = D + 2;             // F column stride
     static constexpr int FE = ACOL * FS;         // F buffer, complex
-    static constexpr int TWS = 18;               // twiddle-table row stride (rows 144 B apart: no bank overlap)
-    static constexpr int TW = 16 * TWS;          // twiddle table W_D^{t m}, t, m < 16
+    static constexpr int TWS = R1 + 2;           // twiddle-table row stride (rows don't overlap banks)
+    static constexpr int TW = 16 * TWS;          // twiddle table W_D^{t m}, t < 16, m < R1
     static constexpr size_t SMEM = (size_t)(XE + FE + TW) * 8;
 };
 
@@ -255,8 +255,7 @@ __device__ __forceinline__ int xslot(int s) { return (((s & 1) << 2) | (s >> 1))
 // too little L1); the caller puts a barrier between tiles.
 //   in:  v[k] = x(t + 16 k) of slot s1, lane t
 //   out: emit(r, y) for r < NR, y[m2] = X(16 r + oi + R1 m2) of slot os
-// The writer applies W_D^{t (m1 mod 16)} (table row tw = W_D^{t *}); the reader of round
-// r = 1 applies the rest, W_D^{16 t} = W_32^t (compile-time constants).  Per round: write
+// The writer applies the whole twiddle W_D^{t m1} (table row tw = W_D^{t *}, R1 entries).  Per round: write
 // 16 values, barrier, read one sequence, barrier (the buffer holds one round).  before_sync
 // runs after this thread's first-round writes, after_sync right after the first barrier
 // (v is dead then unless NR = 2 -- the second-round values live in v[16..31]).
@@ -274,8 +273,8 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
     for (int r = 0; r < NR; ++r) {
 #pragma unroll
         for (int m = 0; m < 16; m += 2) {
-            const float4 w2 = lds128_nohoist(tw4 + (m >> 1));
-            const float2 a = m ? cmw(v[16 * r + m], make_float2(w2.x, w2.y)) : v[16 * r];
+            const float4 w2 = lds128_nohoist(tw4 + ((16 * r + m) >> 1));
+            const float2 a = (r || m) ? cmw(v[16 * r + m], make_float2(w2.x, w2.y)) : v[16 * r];
             const float2 b = cmw(v[16 * r + m + 1], make_float2(w2.z, w2.w));
             xw[17 * m] = a;
             xw[17 * (m + 1)] = b;
@@ -290,10 +289,6 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
         for (int tt = 0; tt < 16; ++tt) y[tt] = xr[tt];
         if (r + 1 < NR) __syncthreads();   // round r + 1 reuses the buffer
         if (r == NR - 1) after_sync();
-        if (r == 1) {
-#pragma unroll
-            for (int tt = 1; tt < 16; ++tt) y[tt] = cmw(y[tt], w32(tt));
-        }
         if (!(dbg & 8)) dft16(y);
         emit(r, y);
     }
@@ -316,8 +311,8 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     //   S1 / M1 (Zak tile, B tiles, stage 1 of product tiles): slot s8 = tid & 7, t / i = h8 = tid >> 3
     //   M3 (stage 2 of product tiles): warp w, lane L: slot 4 (w >> 1) + (L >> 3), i = (L & 7) + 8 (w & 1)
     const int s8 = tid & 7, h8 = tid >> 3;
-    for (int e = tid; e < 16 * 16; e += K::NT) {
-        const int tt = e / 16, m = e % 16;
+    for (int e = tid; e < 16 * R1; e += K::NT) {
+        const int tt = e / R1, m = e % R1;
         double sn, cs;
         sincospi(-2.0 * (double)((tt * m) % D) / (double)D, &sn, &cs);
         twt[tt * K::TWS + m] = make_float2((float)cs, (float)sn);
