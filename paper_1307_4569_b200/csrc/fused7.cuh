@@ -295,7 +295,9 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
     mark(14);
 }
 
-template <int D, int MINB>
+// FULLPF: the whole next tile's inputs are prefetched behind the current tile's stage 2
+// (fits the 168-register budget of 3 CTAs/SM; with 4+ CTAs only the first half).
+template <int D, int MINB, bool FULLPF = (MINB <= 3)>
 __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     using K = Cfg<D>;
     constexpr int R1 = K::R1, Q = K::Q, M = D, AC = K::ACOL, BT = K::BT;
@@ -379,7 +381,10 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     };
     auto prefetch_next = [&]() {
         int isA0, idx0, w0;
-        if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) load_first(isA0, w0, idx0, 0);
+        if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
+            load_first(isA0, w0, idx0, 0);
+            if (FULLPF && R1 > 16) load_first(isA0, w0, idx0, 1);
+        }
     };
     // Completion signals are deferred: thread 0 publishes "job done" (fence + counter add)
     // once it is into its next job's first tile, when the job's stores have drained and
@@ -434,13 +439,17 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
             if (!isA) __syncthreads();
             load_first(isA, w, idx, 0);
         }
-        if (R1 > 16) load_first(isA, w, idx, 1);
+        if (R1 > 16 && (!FULLPF || !pref)) load_first(isA, w, idx, 1);
         mark(pref ? 6 : 5);
         if (isA) {
             // ---------------- pass A: columns j0 .. j0 + 7 ----------------
             const int j0 = idx * AC;
             // Zak DFT of 8 columns: F_j(nu), nu = 16 r + i + R1 m2, stored at F[col * FS + nu]
-            dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, [&] { if (tid == 0) flush(); }, [&] { load_g(j0, 0, 0); },
+            dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, [&] { if (tid == 0) flush(); },
+                        [&] {
+                            load_g(j0, 0, 0);
+                            if (FULLPF && R1 > 16) load_g(j0, 0, 1);
+                        },
                         [&](int r, const float2* y) {
 #pragma unroll
                             for (int m2 = 0; m2 < 16; ++m2) {
@@ -468,8 +477,10 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
 #pragma unroll
                 for (int k = 0; k < 16; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
                 if (R1 > 16) {
-                    asm volatile("" ::: "memory");
-                    load_g(j0, h, 1);
+                    if (!FULLPF) {
+                        asm volatile("" ::: "memory");
+                        load_g(j0, h, 1);
+                    }
 #pragma unroll
                     for (int k = 16; k < R1; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
                 }
@@ -485,7 +496,14 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                 float2* dst = wsl + (int64_t)jM * (Q * D) + (iM >> 2) * 16 + (iM & 3) * 4 + kap;
                 dft_tile<D>(pre, tw, X2, s8, h8, 4 * colM + uM, iM,
                             [&] { if (h == 3 && tid == 0) claim_ready(); },
-                            [&] { if (h < 3) load_g(j0, h + 1, 0); else prefetch_next(); },
+                            [&] {
+                                if (h < 3) {
+                                    load_g(j0, h + 1, 0);
+                                    if (FULLPF && R1 > 16) load_g(j0, h + 1, 1);
+                                } else {
+                                    prefetch_next();
+                                }
+                            },
                             [&](int r, const float2* y) {
                                 if (A.dbg & 4) return;
 #pragma unroll
@@ -502,7 +520,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                 const float2 e = __ldg(A.E + n);
                 float2* dst = A.out + (int64_t)w * M * N + n;
                 if (bt) {
-                    if (R1 > 16) load_ring(w, idx, bt, 1);   // second half (the first was prefetched)
+                    if (!FULLPF && R1 > 16) load_ring(w, idx, bt, 1);   // second half (the first was prefetched)
                     __syncthreads();   // previous tile's readers are done with X
                 }
                 dft_tile<D>(pre, tw, X2, s8, h8, s8, h8,
@@ -513,8 +531,12 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                                 }
                             },
                             [&] {
-                                if (bt + 1 < BT) load_ring(w, idx, bt + 1, 0);
-                                else prefetch_next();
+                                if (bt + 1 < BT) {
+                                    load_ring(w, idx, bt + 1, 0);
+                                    if (FULLPF && R1 > 16) load_ring(w, idx, bt + 1, 1);
+                                } else {
+                                    prefetch_next();
+                                }
                             },
                             [&](int r, const float2* y) {
                                 if (A.dbg & 4) return;
