@@ -196,6 +196,17 @@ __device__ __forceinline__ void spin_until(const int* p, int target) {
     while (ld_acquire(p) < target) __nanosleep(64);
 }
 __device__ __forceinline__ float2 ld_cs(const float2* p) { return __ldcs(p); }
+// read-only streams that are used once per SM: keep them out of L1
+__device__ __forceinline__ float4 ldg_na(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float2 ldg_na2(const float2* p) {
+    float2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+    return r;
+}
 // shared-memory 16-byte load the compiler may not hoist out of loops (the twiddle table is
 // loop-invariant; hoisting it costs 32 registers)
 __device__ __forceinline__ float4 lds128_nohoist(const float4* p) {
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     auto load_f = [&](int w, int j0, int b) {   // Zak DFT input: column j0 + s8, rows t + 16 k
         const float2* fw = A.f + (int64_t)w * M * D + j0 + s8;
 #pragma unroll
-        for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ld_cs(fw + (int64_t)(h8 + 16 * k) * M);
+        for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ldg_na2(fw + (int64_t)(h8 + 16 * k) * M);
     };
     // G' of product tile h (slot s8 = 4 col + u, lane t).  Layout [j0 / 8][h][kp][t][slot] of
     // float4 (k = 2 kp, 2 kp + 1): a warp reads 512 contiguous bytes.
@@ -349,7 +360,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
         const float4* G4 = A.Gp + ((int64_t)((j0 / AC) * 4 + h) * (R1 / 2)) * 128 + h8 * 8 + s8;
 #pragma unroll
         for (int kp = 8 * b; kp < 8 * b + 8 && kp < R1 / 2; ++kp) {
-            const float4 g = __ldg(G4 + kp * 128);
+            const float4 g = ldg_na(G4 + kp * 128);
             pre[2 * kp] = make_float2(g.x, g.y);
             pre[2 * kp + 1] = make_float2(g.z, g.w);
         }
