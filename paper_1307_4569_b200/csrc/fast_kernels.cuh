@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -744,6 +745,8 @@ int build_fast7(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, cons
     if (const char* e = std::getenv("NSDGT_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     fp->grid = per_sm * sms;
     fp->smem = smem;
+    if (std::getenv("NSDGT_VERBOSE"))
+        std::fprintf(stderr, "fused7: D=%d CTAs/SM=%d grid=%d smem/CTA=%zu B S=%d\n", (int)D, per_sm, fp->grid, smem, fp->S7);
     fp->D = (int)D; fp->MM = (int)M; fp->Q = (int)Q; fp->c = (int)I.c; fp->N = (int)N; fp->L = L;
     fp->nA = (int)(M / v7::Cfg<512>::ACOL); fp->nB = (int)(N / 16);
     fp->Kmod = (int)(K % D);
