@@ -570,12 +570,8 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
                                                          I.s1, I.a_r);
     }
     CUDA_TRY(cudaGetLastError());
-    int rc = build_fast<T>(&P->fp, P->info, P->G, P->chirp, P->E, P->rot, (P->flags & DGT_FORCE_GENERIC) != 0, st);
+    int rc = build_fast<T>(&P->fp, P->info, gt, P->E, (P->flags & DGT_FORCE_GENERIC) != 0, st);
     if (rc) return rc;
-    if (!(P->flags & DGT_FORCE_GENERIC)) {
-        rc = build_fast7<T>(&P->fp, P->info, gt, P->E, st);
-        if (rc) return rc;
-    }
     P->fast = P->fp.kind;
     CUDA_TRY(cudaStreamSynchronize(st));
     cudaFree(g_dev);

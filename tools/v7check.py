@@ -22,12 +22,9 @@ for k, Wt in [(3, 256), (5, 1024)]:
     W = 5
     f = batch(wl, 0, W)
     ft = torch.from_numpy(f).cuda()
-    os.environ.pop("NSDGT_V6", None)
     p7 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
-    os.environ["NSDGT_V6"] = "1"
-    p6 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
-    os.environ.pop("NSDGT_V6", None)
-    print(f"cfg{k}: v7 kernel_path={p7.info['kernel_path']} v6 kernel_path={p6.info['kernel_path']}", flush=True)
+    p6 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, force_generic=True)   # "v6" = generic reference
+    print(f"cfg{k}: fused7 kernel_path={p7.info['kernel_path']} generic kernel_path={p6.info['kernel_path']}", flush=True)
     c7 = p7.execute(ft).cpu().numpy()
     c6 = p6.execute(ft).cpu().numpy()
     print(f"  rel(v7, v6) = {rel(c7, c6):.3e}", flush=True)

@@ -10,7 +10,7 @@ fb = torch.randn(Wt, wl.L, dtype=torch.complex64, device="cuda")
 cb = torch.empty(Wt, wl.M, wl.N, dtype=torch.complex64, device="cuda")
 settings = [(x.split(":") + ["1"])[:3] for x in os.environ.get("SETS", "4:2,6:4,8:6,3:1,2:1").split(",")]
 for S, lag, pers in settings:
-    os.environ["NSDGT_S"], os.environ["NSDGT_LAG"], os.environ["NSDGT_PERSIST"] = S, lag, pers
+    os.environ["NSDGT_S"], os.environ["NSDGT_LAG"] = S, lag
     p = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
     for _ in range(2): p.execute(fb, out=cb)
     torch.cuda.synchronize()
