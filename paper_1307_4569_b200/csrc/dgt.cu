@@ -818,9 +818,12 @@ int dgt_execute_host(dgt_plan_t plan, const void* f_host, void* c_host, int64_t 
     const dgt_lattice_info& I = P->info;
     const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
     const size_t per_f = (size_t)I.L * ein, per_c = (size_t)I.M * I.N * P->esz;
-    // staging chunk: a multiple of the compute chunk, ~256 MB of output per slot
-    int64_t sw = std::max<int64_t>(1, (int64_t)((256ull << 20) / per_c));
-    sw = std::max<int64_t>(P->chunk, sw / P->chunk * P->chunk);
+    // staging chunk: ~128 MB of output per slot (flat from 32 to 512 MB on cfg5: the two
+    // copy directions overlap each other and the kernels at the PCIe floor)
+    int64_t sw = std::max<int64_t>(1, (int64_t)((128ull << 20) / per_c));
+    // a multiple of the compute chunk when that is smaller (the fused path has no chunk
+    // limit: P->chunk is then huge and the staging size alone decides)
+    if (P->chunk < sw) sw = sw / P->chunk * P->chunk;
     sw = std::min<int64_t>(sw, W);
     if (!P->s_in) {
         CUDA_TRY(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
