@@ -199,6 +199,7 @@ struct ZakArgs {
     void* C;            // intermediate [W][iM][q][d]
     int64_t L, c, d, p, q, iM;
     int RB;
+    int allu;           // p = 1: products and DFT_d of all q values of u in one pass (smem 2 q RB d)
     Radices rd;
     const void* tw;     // twiddles of length d
 };
@@ -243,6 +244,37 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
         bufA[(rr * pi + k) * di + s] = v;
     }
     __syncthreads();
+    if (A.allu) {
+        // p = 1, all u at once: DFT_d of the nr gathered columns, the q nr products, one
+        // batched DFT_d of q nr sequences, one scatter (3 barrier-separated phases of q x
+        // the work instead of q rounds of products + DFT + scatter).  Buffers: two regions of
+        // q RB d; Phi lives in the first nr d of one of them.
+        C* R1 = bufA;
+        C* R2 = bufA + (size_t)qi * RB * d;
+        C* phi = fft_smem<T>(R1, R2, A.rd, nr, di, tw);
+        C* Yb = (phi == R1) ? R2 : R1;
+        const C* __restrict__ G = (const C*)A.G;
+        const int nrd = nr * di;
+        for (int i = threadIdx.x; i < qi * nrd; i += blockDim.x) {
+            const int u = i / nrd, rem = i - u * nrd;
+            const int rr = rem / di, nu = rem - rr * di;
+            Yb[i] = cmul(phi[rem], G[(((int)r0 + rr) * qi + u) * di + nu]);
+        }
+        __syncthreads();
+        C* Y = fft_smem<T>(Yb, phi, A.rd, qi * nr, di, tw);
+        C* Cw = (C*)A.C + w * A.iM * q * d;
+        const int jbase = (int)(r0 + c * ((l * p) % q));
+        for (int i = threadIdx.x; i < qi * nrd; i += blockDim.x) {
+            const int u = i / nrd, rem = i - u * nrd;
+            const int rr = rem / di, np = rem - rr * di;
+            const int kappa = ((l - u) % qi + qi) % qi;
+            int tau = di - np - (l < u ? 1 : 0);       // (-n' - [l < u]) mod d
+            if (tau >= di) tau -= di;
+            if (tau < 0) tau += di;
+            Cw[((jbase + rr) * qi + kappa) * di + np] = Y[(u * nr + rr) * di + tau];
+        }
+        return;
+    }
     // 2. DFT_d over s for nr*p sequences
     C* phi = fft_smem<T>(bufA, bufB, A.rd, nr * (int)p, (int)d, tw);
     C* free0 = (phi == bufA) ? bufB : bufA;
@@ -284,7 +316,8 @@ struct OutArgs {
     const void* C;  // [W][iM][q][d]
     void* out;      // [W][M][N]
     int64_t iM, iN, q, d;
-    int NT;         // columns (consecutive inner n) per CTA
+    int NT;         // columns per CTA: T-branch consecutive inner n; F-branch (grouped) n = kappa + q (n'0 + i)
+    int grouped;    // 1: CTA x = (kappa, block of NT consecutive n'), contiguous loads
     Radices rd;
     const void* tw;  // twiddles of length iM
     int branch;
@@ -295,7 +328,9 @@ struct OutArgs {
     // F-branch
     const void* ptab;
     int64_t L, b, Nr, ar, s1, C1, C2, C3, C4, C5, C6;
-    const int* ktab;               // per inner channel k < N_r: [C1 k mod 2N | C5 k mod 2N | (-s1 a_r k) mod L]
+    int64_t sar;                   // (-s1 a_r) mod L
+    unsigned int D1, D5, DX;       // 256 C1 mod 2N, 256 C5 mod 2N, 256 sar mod L (k -> k - 256)
+    unsigned int invb;             // floor((2^32 - 1) / b)
     unsigned long long inv2N, invL;   // Barrett constants floor(2^64 / 2N), floor(2^64 / L)
 };
 
@@ -309,14 +344,89 @@ __device__ __forceinline__ unsigned int bmod(unsigned long long x, unsigned int 
     return (unsigned int)r;
 }
 
-// F-branch per-channel table (plan time, exact integers)
-__global__ void k_fbranch_ktab(int* kt, int64_t Nr, int64_t twoN, int64_t L, int64_t C1, int64_t C5, int64_t s1,
-                               int64_t ar) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < Nr; k += (int64_t)gridDim.x * blockDim.x) {
-        kt[k] = (int)((((unsigned __int128)C1 * k) % twoN));
-        kt[Nr + k] = (int)((((unsigned __int128)C5 * k) % twoN));
-        const __int128 v = -(((__int128)(s1 % L) * (((__int128)ar * k) % L)) % L);
-        kt[2 * Nr + k] = (int)(((v % L) + L) % L);
+// F-branch output remap (Alg. 1 lines 24-31): c[kt][mt] = E(k,m) c_r[(-k) mod N_r][m]; the
+// inner channel is the FFT output index kc = (-k) mod N_r, the inner time index m = n.
+//   sq = (C1 k + C2 m) mod 2N,  e = (C3 sq^2 - m (C4 m + C5 k)) mod 2N,
+//   mt = sq mod N,  kt = ((-s1 a_r k + C6 m) mod L) div b
+// The k-dependent residues come from the plan's per-channel table, the m-dependent ones
+// are per-column constants; every reduction is exact (Barrett, 64-bit products).
+struct FbCol {
+    unsigned int mD, mA, mC4, mT;
+};
+__device__ __forceinline__ FbCol fb_col(const OutArgs& A, unsigned long long m) {
+    const unsigned int twoN = (unsigned int)(2 * A.N), Lu = (unsigned int)A.L;
+    FbCol c;
+    c.mD = bmod(m, twoN, A.inv2N);
+    c.mA = bmod((unsigned long long)A.C2 * c.mD, twoN, A.inv2N);
+    c.mC4 = bmod((unsigned long long)A.C4 * c.mD, twoN, A.inv2N);
+    c.mT = bmod((unsigned long long)(A.C6 % A.L) * (m % A.L), Lu, A.invL);
+    return c;
+}
+__device__ __forceinline__ unsigned int submod(unsigned int x, unsigned int dlt, unsigned int m) {
+    return x >= dlt ? x - dlt : x + m - dlt;
+}
+// The residues of one column along kc, kc + 256, kc + 512, ... (k = N_r - kc decreases by
+// 256 per step): sq = (C1 k + C2 m) mod 2N, uu = (C4 m + C5 k) mod 2N, t2 = m uu mod 2N and
+// xx = (-s1 a_r k + C6 m) mod L are affine in k, so each step is a subtraction mod 2N / L
+// (the deltas D1 = 256 C1, D5 = 256 C5, DX = 256 (-s1 a_r) are plan constants); only the
+// C3 sq^2 term (0 for config 4) needs a product per coefficient.
+struct FbIter {
+    unsigned int sq, uu, t2, xx, dt2;
+};
+__device__ __forceinline__ FbIter fb_iter(const OutArgs& A, const FbCol& cc, unsigned long long k) {
+    const unsigned int twoN = (unsigned int)(2 * A.N), Lu = (unsigned int)A.L;
+    FbIter it;
+    it.sq = bmod((unsigned long long)A.C1 * k, twoN, A.inv2N) + cc.mA;
+    if (it.sq >= twoN) it.sq -= twoN;
+    it.uu = cc.mC4 + bmod((unsigned long long)A.C5 * k, twoN, A.inv2N);
+    if (it.uu >= twoN) it.uu -= twoN;
+    it.t2 = bmod((unsigned long long)cc.mD * it.uu, twoN, A.inv2N);
+    it.xx = (A.sar ? bmod((unsigned long long)A.sar * k, Lu, A.invL) : 0u) + cc.mT;
+    if (it.xx >= Lu) it.xx -= Lu;
+    it.dt2 = bmod((unsigned long long)cc.mD * A.D5, twoN, A.inv2N);
+    return it;
+}
+__device__ __forceinline__ void fb_step(const OutArgs& A, FbIter& it) {
+    const unsigned int twoN = (unsigned int)(2 * A.N);
+    it.sq = submod(it.sq, A.D1, twoN);
+    it.uu = submod(it.uu, A.D5, twoN);
+    it.t2 = submod(it.t2, it.dt2, twoN);
+    it.xx = submod(it.xx, A.DX, (unsigned int)A.L);
+}
+template <typename C>
+__device__ __forceinline__ void fb_put(const OutArgs& A, C* out, const FbIter& it, C val) {
+    const unsigned int twoN = (unsigned int)(2 * A.N), Nn = (unsigned int)A.N;
+    unsigned int t1 = 0;
+    if (A.C3) {
+        const unsigned int s2 = bmod((unsigned long long)it.sq * it.sq, twoN, A.inv2N);
+        t1 = bmod((unsigned long long)A.C3 * s2, twoN, A.inv2N);
+    }
+    const unsigned int e = submod(t1, it.t2, twoN);
+    const unsigned int mt = it.sq >= Nn ? it.sq - Nn : it.sq;
+    // kt = xx div b (32-bit Barrett, two corrections)
+    const unsigned int bu = (unsigned int)A.b;
+    unsigned int kt = __umulhi(it.xx, A.invb);
+    unsigned int r = it.xx - kt * bu;
+    if (r >= bu) { r -= bu; ++kt; }
+    if (r >= bu) ++kt;
+    out[(size_t)kt * Nn + mt] = cmul(__ldg((const C*)A.ptab + e), val);
+}
+// column m, coefficients kc = kc0 + 256 i, i < cnt (kc0 < 256; CNT > 0: compile-time count,
+// fully unrolled so get(i) may index registers)
+template <int CNT, typename C, class Get>
+__device__ __forceinline__ void fb_column(const OutArgs& A, C* out, unsigned long long m, unsigned int kc0, int cnt,
+                                          Get&& get) {
+    const FbCol cc = fb_col(A, m);
+    const int n = CNT > 0 ? CNT : cnt;
+    if (n <= 0) return;
+    // k = N_r - kc for kc > 0, k = 0 for kc = 0 (then the sequence restarts at N_r - 256)
+    FbIter it = fb_iter(A, cc, kc0 ? (unsigned long long)A.Nr - kc0 : 0ull);
+#pragma unroll
+    for (int i = 0; i < (CNT > 0 ? CNT : 1 << 30); ++i) {
+        if (CNT <= 0 && i >= n) break;
+        if (i == 1 && kc0 == 0) it = fb_iter(A, cc, (unsigned long long)A.Nr - 256u);
+        else if (i > 0) fb_step(A, it);
+        fb_put(A, out, it, get(i));
     }
 }
 
@@ -326,20 +436,50 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
     using C = cx<T>;
     const int64_t iM = A.iM, iN = A.iN, q = A.q, d = A.d;
     const int NT = A.NT;
-    const int64_t n0 = (int64_t)blockIdx.x * NT;
-    const int nt = (int)((iN - n0) < NT ? (iN - n0) : NT);
+    const int iMi = (int)iM, qi = (int)q, di = (int)d;
+    // column cl of this CTA is inner n = nb + ns * cl: T-branch nb = x NT, ns = 1 (consecutive
+    // n, coalesced stores); F-branch grouped: x = kappa + q * blk, nb = kappa + q NT blk,
+    // ns = q, so C(j, n) = [j][kappa][n'] is contiguous over cl (the F-branch stores are
+    // scattered by the remap anyway)
+    int64_t nb, ns;
+    int nt;
+    if (A.grouped) {
+        const int kap = (int)(blockIdx.x % q), blk = (int)(blockIdx.x / q);
+        nb = kap + q * (int64_t)blk * NT;
+        ns = q;
+        nt = (int)((d - (int64_t)blk * NT) < NT ? (d - (int64_t)blk * NT) : NT);
+    } else {
+        nb = (int64_t)blockIdx.x * NT;
+        ns = 1;
+        nt = (int)((iN - nb) < NT ? (iN - nb) : NT);
+    }
     const int64_t w = blockIdx.y;
     C* bufA = (C*)smem_raw;
     C* bufB = bufA + (size_t)NT * iM;
     const C* __restrict__ Cin = (const C*)A.C + w * iM * iN;
-    const int iMi = (int)iM, qi = (int)q, di = (int)d;
-    // load columns n0..n0+nt: C(j, n) stored at [j][n mod q][n div q] (32-bit indices within a signal)
-    for (int i = threadIdx.x; i < nt * iMi; i += blockDim.x) {
-        const int cl = i % nt;
-        const int j = i / nt;
-        const int n = (int)n0 + cl;
-        const int nq = n / qi;
-        bufA[cl * iMi + j] = Cin[(j * qi + (n - nq * qi)) * di + nq];
+    // load columns: C(j, n) stored at [j][n mod q][n div q] (32-bit indices within a signal);
+    // eight independent loads in flight per thread
+    {
+        const int total = nt * iMi, nbi = (int)nb, nsi = (int)ns;
+        constexpr int U = 8;
+        for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+            C v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < total) {
+                    const int cl = i % nt, j = i / nt;
+                    const int n = nbi + nsi * cl;
+                    const int nq = n / qi;
+                    v[u] = Cin[(j * qi + (n - nq * qi)) * di + nq];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < total) bufA[(i % nt) * iMi + i / nt] = v[u];
+            }
+        }
     }
     __syncthreads();
     C* X = fft_smem<T>(bufA, bufB, A.rd, nt, (int)iM, (const C*)A.tw);
@@ -351,51 +491,81 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
         for (int i = threadIdx.x; i < nt * iMi; i += blockDim.x) {
             const int cl = i % nt;
             const int mo = i / nt;
-            const int n = (int)n0 + cl;
+            const int n = (int)nb + cl;
             int m = mo + A.rot[n];
             if (m >= Mi) m -= Mi;
             out[mo * Ni + n] = cmul(E[n], X[cl * iMi + m]);
         }
     } else {
-        // c[kt][mt] = E(k,m) c_r[(-k) mod N_r][m]  (Alg. 1 lines 24-31); here the inner
-        // channel is the FFT output index kc = (-k) mod N_r, the inner time index m = n.
-        //   sq = (C1 k + C2 m) mod 2N,  e = (C3 sq^2 - m (C4 m + C5 k)) mod 2N,
-        //   mt = sq mod N,  kt = ((-s1 a_r k + C6 m) mod L) div b
-        // The k-dependent residues come from the plan's per-channel table, the m-dependent
-        // ones are per-column constants; every reduction is exact (Barrett, 64-bit products).
         C* out = (C*)A.out + w * A.M * A.N;
-        const C* P = (const C*)A.ptab;
-        const unsigned int twoN = (unsigned int)(2 * A.N), Nn = (unsigned int)A.N, Lu = (unsigned int)A.L;
-        const unsigned int bu = (unsigned int)A.b, Nr = (unsigned int)A.Nr;
-        const int* kA = A.ktab;
-        const int* kC = A.ktab + A.Nr;
-        const int* kT = A.ktab + 2 * A.Nr;
         for (int cl = 0; cl < nt; ++cl) {
-            const unsigned long long m = (unsigned long long)(n0 + cl);
-            const unsigned int mD = bmod(m, twoN, A.inv2N);
-            const unsigned int mA = bmod((unsigned long long)A.C2 * mD, twoN, A.inv2N);
-            const unsigned int mC4 = bmod((unsigned long long)A.C4 * mD, twoN, A.inv2N);
-            const unsigned int mT = bmod((unsigned long long)(A.C6 % A.L) * (m % A.L), Lu, A.invL);
             const C* Xc = X + cl * iMi;
-            for (int kc = threadIdx.x; kc < iMi; kc += blockDim.x) {
-                const unsigned int k = kc ? Nr - (unsigned int)kc : 0u;
-                unsigned int sq = (unsigned int)kA[k] + mA;
-                if (sq >= twoN) sq -= twoN;
-                const unsigned int s2 = bmod((unsigned long long)sq * sq, twoN, A.inv2N);
-                const unsigned int t1 = bmod((unsigned long long)A.C3 * s2, twoN, A.inv2N);
-                unsigned int uu = mC4 + (unsigned int)kC[k];
-                if (uu >= twoN) uu -= twoN;
-                const unsigned int t2 = bmod((unsigned long long)mD * uu, twoN, A.inv2N);
-                const unsigned int e = t1 >= t2 ? t1 - t2 : t1 + twoN - t2;
-                const unsigned int mt = sq >= Nn ? sq - Nn : sq;
-                unsigned int xx = (unsigned int)kT[k] + mT;
-                if (xx >= Lu) xx -= Lu;
-                const unsigned int kt = xx / bu;
-                out[(size_t)kt * Nn + mt] = cmul(P[e], Xc[kc]);
-            }
+            const int kc0 = threadIdx.x;   // blockDim.x == 256
+            fb_column<0>(A, out, (unsigned long long)(nb + ns * cl), (unsigned int)kc0, (iMi - kc0 + 255) / 256,
+                      [&](int i) { return Xc[kc0 + 256 * i]; });
         }
     }
 }
+
+// F-branch output kernel for N_r = iM = 4096 = 16^3 (config 4): one CTA of 256 threads per
+// inner column m.  Three register radix-16 passes with two shared-memory exchanges in one
+// padded buffer (16 x 272 elements) instead of three Stockham ping-pong passes over two
+// full-column buffers: 70 KB (c128) per CTA, so 3 CTAs share an SM; the 16 loads of pass 1
+// come straight from the intermediate C[w][j][kappa][n'] (j = t + 256 r).
+//   pass 1 (lane t):         Y(t, k1)  = W_4096^{t k1} sum_r x(t + 256 r) W_16^{r k1}
+//   pass 2 (lane k1, t1):    Z(k1, t1, k2) = W_256^{t1 k2} sum_t2 Y(t1 + 16 t2, k1) W_16^{t2 k2}
+//   pass 3 (lane k1, k2):    X(k1 + 16 k2 + 256 k3) = sum_t1 Z(k1, t1, k2) W_16^{t1 k3}
+// v[k] *= W_4096^{s k}, k = 1..15, from four table loads (W^s, W^2s, W^4s, W^8s) and eleven
+// products (at most three roundings per twiddle; fifteen scattered loads per lane was the
+// kernel's largest L1 cost)
+template <typename C>
+__device__ __forceinline__ void twiddle15(C* v, const C* __restrict__ tw, int s) {
+    const C w1 = __ldg(tw + (s & 4095)), w2 = __ldg(tw + ((2 * s) & 4095));
+    const C w4 = __ldg(tw + ((4 * s) & 4095)), w8 = __ldg(tw + ((8 * s) & 4095));
+    const C w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+    v[1] = cmul(v[1], w1); v[2] = cmul(v[2], w2); v[3] = cmul(v[3], w3); v[4] = cmul(v[4], w4);
+    v[5] = cmul(v[5], w5); v[6] = cmul(v[6], w6); v[7] = cmul(v[7], w7); v[8] = cmul(v[8], w8);
+    v[9] = cmul(v[9], cmul(w1, w8)); v[10] = cmul(v[10], cmul(w2, w8)); v[11] = cmul(v[11], cmul(w3, w8));
+    v[12] = cmul(v[12], cmul(w4, w8)); v[13] = cmul(v[13], cmul(w5, w8)); v[14] = cmul(v[14], cmul(w6, w8));
+    v[15] = cmul(v[15], cmul(w7, w8));
+}
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(256, MINB) out_f4096_kernel(OutArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using C = cx<T>;
+    C* S = (C*)smem_raw;
+    const int tid = threadIdx.x;
+    const int m = blockIdx.x;              // inner column
+    const int64_t w = blockIdx.y;
+    const int qi = (int)A.q, di = (int)A.d;
+    const C* __restrict__ src = (const C*)A.C + w * A.iM * A.iN + (m % qi) * di + m / qi;
+    const C* __restrict__ tw = (const C*)A.tw;
+    const int ld = qi * di;                // row stride of C over j
+    C v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = src[(tid + 256 * r) * ld];
+    dft16<T>(v);
+    twiddle15(v, tw, tid);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) S[k * 256 + tid] = v[k];
+    __syncthreads();
+    const int hi = tid >> 4, lo = tid & 15;   // pass 2: (k1, t1); pass 3: (k1, k2)
+#pragma unroll
+    for (int t2 = 0; t2 < 16; ++t2) v[t2] = S[hi * 256 + lo + 16 * t2];
+    __syncthreads();
+    dft16<T>(v);
+    twiddle15(v, tw, 16 * lo);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) S[hi * 272 + 17 * k + lo] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int t1 = 0; t1 < 16; ++t1) v[t1] = S[hi * 272 + 17 * lo + t1];
+    dft16<T>(v);
+    C* out = (C*)A.out + w * A.M * A.N;
+    fb_column<16>(A, out, (unsigned long long)m, (unsigned int)(hi + 16 * lo), 16, [&](int i) { return v[i]; });
+}
+constexpr size_t kOutF4096Elems = 16 * 272;
 
 // ---------------------------------------------------------------------------------
 // the plan
@@ -416,7 +586,6 @@ struct Plan {
     void* E = nullptr;       // T-branch column phases (N)
     int* rot = nullptr;      // T-branch rotations (N)
     void* ptab = nullptr;    // F-branch phase table (2N)
-    int* ktab = nullptr;     // F-branch per-channel residues (3 N_r)
     // workspace
     void* Cws = nullptr;     // chunk intermediate
     void* fhat = nullptr;    // F-branch chunk spectra
@@ -427,6 +596,8 @@ struct Plan {
     Radices rd_d{}, rd_m{};
     int RB = 1, NT = 1;
     size_t smemA = 0, smemB = 0;
+    int allu = 0;            // zak_kernel all-u mode (p = 1)
+    int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
     int fast = 0;  // specialised path id (0 = generic)
     FastPlan fp{};
     // host pipeline (dgt_execute_host)
@@ -479,7 +650,7 @@ static void prof_close(Plan* P, int h, int kind, double bytes, double flops, cud
 
 static void free_plan(Plan* P) {
     if (!P) return;
-    void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->ktab, P->Cws, P->fhat,
+    void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
                     P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1]};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -565,9 +736,6 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
     } else {
         CUDA_TRY(cudaMalloc(&P->ptab, sizeof(C) * 2 * I.N));
         k_phase_table<T><<<grid_for(2 * I.N), 256, 0, st>>>((C*)P->ptab, I.N);
-        CUDA_TRY(cudaMalloc(&P->ktab, sizeof(int) * 3 * I.N_r));
-        k_fbranch_ktab<<<grid_for(I.N_r), 256, 0, st>>>(P->ktab, I.N_r, 2 * I.N, I.L, I.C1 % (2 * I.N), I.C5 % (2 * I.N),
-                                                         I.s1, I.a_r);
     }
     CUDA_TRY(cudaGetLastError());
     int rc = build_fast<T>(&P->fp, P->info, gt, P->E, (P->flags & DGT_FORCE_GENERIC) != 0, st);
@@ -626,7 +794,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     ZakArgs A{};
     A.f = src; A.real_in = real_src; A.chirp = P->chirp; A.G = P->G; A.C = P->Cws;
     A.L = I.L; A.c = I.c; A.d = I.d; A.p = I.p; A.q = I.q; A.iM = I.iM;
-    A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d;
+    A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = P->allu;
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
     zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
@@ -634,6 +802,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     OutArgs B{};
     B.C = P->Cws; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
     B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
+    B.grouped = I.branch == DGT_BRANCH_FREQ ? 1 : 0;
     B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
     B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
     {
@@ -642,12 +811,21 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
         B.C1 = nm(I.C1, twoN); B.C2 = nm(I.C2, twoN); B.C3 = nm(I.C3, twoN); B.C4 = nm(I.C4, twoN);
         B.C5 = nm(I.C5, twoN); B.C6 = nm(I.C6, I.L);
     }
-    B.ktab = P->ktab;
+    B.sar = (((-(I.s1 % I.L)) * (I.a_r % I.L)) % I.L + I.L) % I.L;
+    B.D1 = (unsigned int)((256 * B.C1) % (2 * I.N));
+    B.D5 = (unsigned int)((256 * B.C5) % (2 * I.N));
+    B.DX = (unsigned int)(((__int128)256 * B.sar) % I.L);
+    B.invb = (unsigned int)(0xffffffffull / (unsigned long long)I.b);
     B.inv2N = ~0ull / (unsigned long long)(2 * I.N);
     B.invL = ~0ull / (unsigned long long)I.L;
-    const int ntiles = (int)((I.iN + P->NT - 1) / P->NT);
+    const int ntiles = B.grouped ? (int)(I.q * ((I.d + P->NT - 1) / P->NT)) : (int)((I.iN + P->NT - 1) / P->NT);
     ph = prof_open(P, st);
-    out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
+    if (P->outk == 1)
+        out_f4096_kernel<T, 3><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+    else if (P->outk == 2)
+        out_f4096_kernel<T, 2><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+    else
+        out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
     prof_close(P, ph, PK_OUT, by_out, fl_out, st);
     CUDA_TRY(cudaGetLastError());
     return DGT_OK;
@@ -678,8 +856,18 @@ static int configure(Plan* P, int64_t max_chunk) {
         return fail(DGT_EUNSUPPORTED, "inner Zak length d=" + std::to_string(I.d) + " too large for shared memory");
     P->RB = rb;
     P->smemA = smemA(rb);
+    // p = 1: all-u mode when two regions of q RB d fit (config 4: 92 KB, 2 CTAs per SM)
+    const size_t smem_allu = (size_t)2 * I.q * rb * I.d * e;
+    if (I.p == 1 && smem_allu <= budget && !std::getenv("NSDGT_ZAK_PERU")) {
+        P->allu = 1;
+        P->smemA = std::max(P->smemA, smem_allu);
+    }
     auto smemB = [&](int nt) { return (size_t)2 * nt * I.iM * e; };
     int nt = (int)std::min<int64_t>(I.iN, 16);
+    // long columns: keep >= 2 CTAs per SM (config 4: 2 x 4096 x 16 B per column, NT = 4 left
+    // one CTA of 8 warps per SM, latency-bound on its loads)
+    while (nt > 1 && smemB(nt) > budget / 2 && smemB(nt) > 48 * 1024) --nt;
+    if (const char* ev = std::getenv("NSDGT_OUT_NT")) nt = std::max(1, std::atoi(ev));   // experiment
     while (nt > 1 && smemB(nt) > budget) --nt;
     if (smemB(nt) > budget)
         return fail(DGT_EUNSUPPORTED, "inner channel count " + std::to_string(I.iM) + " too large for shared memory");
@@ -687,6 +875,14 @@ static int configure(Plan* P, int64_t max_chunk) {
     P->smemB = smemB(nt);
     CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
+    // out_f4096: 2 CTAs per SM for c128 (128 registers, measured faster than 3 CTAs at 80
+    // registers with spills), 3 for c64
+    P->outk = (I.branch == DGT_BRANCH_FREQ && I.iM == 4096 && !std::getenv("NSDGT_OUT_GENERIC")) ? (e == 16 ? 2 : 1) : 0;
+    if (P->outk && std::getenv("NSDGT_OUTF_MINB")) P->outk = std::atoi(std::getenv("NSDGT_OUTF_MINB")) == 2 ? 2 : 1;   // experiment
+    CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kOutF4096Elems * e)));
+    CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kOutF4096Elems * e)));
     // chunk: intermediate of a chunk stays well inside L2
     const size_t per_sig = (size_t)I.iM * I.iN * e;
     int64_t ch = std::max<int64_t>(1, (int64_t)((size_t)(l2 > 0 ? l2 : (64 << 20)) * 2 / 5 / per_sig));

@@ -169,6 +169,26 @@ def test_delta_window_full_size(torch_cuda, nsdgt, k):
         assert rel(c[w], ref) <= TOL[wl.dtype]
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_fbranch_out4096_kernel(torch_cuda, nsdgt, oracle_mod, dtype, monkeypatch):
+    """Frequency shear with N_r = 4096 inner channels takes the out_f4096 kernel (config 4's
+    output kernel): full comparison on a lattice the oracle finishes in seconds, and
+    agreement with the generic Stockham output kernel."""
+    torch = torch_cuda
+    L, a, M, l1, l2 = 36864, 3, 12, 1, 3
+    info = nsdgt.lattice_plan(L, a, M, l1, l2)
+    assert info["branch"] == 2 and info["iM"] == 4096
+    f, g = random_pair(L, 41, dtype=dtype)
+    f2, _ = random_pair(L, 42, dtype=dtype)
+    fb = np.stack([f, f2])
+    c, _ = run_gpu(nsdgt, torch, fb, g, L, a, M, l1, l2, dtype)
+    ref = oracle_mod.dgt(fb, g, a, M, l1, l2)
+    assert rel(c, ref) <= TOL[dtype]
+    monkeypatch.setenv("NSDGT_OUT_GENERIC", "1")
+    cg, _ = run_gpu(nsdgt, torch, fb, g, L, a, M, l1, l2, dtype)
+    assert rel(c, cg) <= TOL[dtype]
+
+
 def test_chunking_ragged_and_host_path(torch_cuda, nsdgt):
     """Ragged chunks (W not a multiple of the chunk), W = 0, and the host end-to-end path
     give bitwise the same result as one device execute."""
