@@ -204,7 +204,8 @@ struct ZakArgs {
     const void* tw;     // twiddles of length d
 };
 
-template <typename T>
+// DCT > 0: compile-time inner length d = DCT (all-u mode only), DFTs by fft_ct
+template <typename T, int DCT>
 __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
     // 1. gather f~(x(r,k,l,s)), x = r + c((k q + p l + s p q) mod (L/c)), rr fastest.
     //    32-bit index arithmetic within a signal (the host checks L < 2^31).
     const int ng = nr * (int)p * (int)d;
-    const int di = (int)d, pi = (int)p, qi = (int)q, ci = (int)c, Lci = (int)Lc;
+    const int di = DCT ? DCT : (int)d, pi = (int)p, qi = (int)q, ci = (int)c, Lci = (int)Lc;
     const int base_kq = pi * l;                     // p l
     const T* fr = (const T*)A.f + w * L;            // real input
     const C* fc = (const C*)A.f + w * L;
@@ -251,7 +252,9 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
         // q RB d; Phi lives in the first nr d of one of them.
         C* R1 = bufA;
         C* R2 = bufA + (size_t)qi * RB * d;
-        C* phi = fft_smem<T>(R1, R2, A.rd, nr, di, tw);
+        C* phi;
+        if constexpr (DCT > 0) phi = fft_ct<T, DCT>(R1, R2, nr, tw);
+        else phi = fft_smem<T>(R1, R2, A.rd, nr, di, tw);
         C* Yb = (phi == R1) ? R2 : R1;
         const C* __restrict__ G = (const C*)A.G;
         const int nrd = nr * di;
@@ -261,7 +264,9 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
             Yb[i] = cmul(phi[rem], G[(((int)r0 + rr) * qi + u) * di + nu]);
         }
         __syncthreads();
-        C* Y = fft_smem<T>(Yb, phi, A.rd, qi * nr, di, tw);
+        C* Y;
+        if constexpr (DCT > 0) Y = fft_ct<T, DCT>(Yb, phi, qi * nr, tw);
+        else Y = fft_smem<T>(Yb, phi, A.rd, qi * nr, di, tw);
         C* Cw = (C*)A.C + w * A.iM * q * d;
         const int jbase = (int)(r0 + c * ((l * p) % q));
         for (int i = threadIdx.x; i < qi * nrd; i += blockDim.x) {
@@ -275,6 +280,7 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
         }
         return;
     }
+    if constexpr (DCT > 0) return;   // compile-time lengths run the all-u mode only
     // 2. DFT_d over s for nr*p sequences
     C* phi = fft_smem<T>(bufA, bufB, A.rd, nr * (int)p, (int)d, tw);
     C* free0 = (phi == bufA) ? bufB : bufA;
@@ -597,6 +603,7 @@ struct Plan {
     int RB = 1, NT = 1;
     size_t smemA = 0, smemB = 0;
     int allu = 0;            // zak_kernel all-u mode (p = 1)
+    int zct = 0;             // zak_kernel compile-time inner length (0 = runtime radices)
     int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
     int fast = 0;  // specialised path id (0 = generic)
     FastPlan fp{};
@@ -797,7 +804,10 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = P->allu;
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
-    zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+    if (P->zct == 180)
+        zak_kernel<T, 180><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+    else
+        zak_kernel<T, 0><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     prof_close(P, ph, PK_ZAK, by_in, fl_zak, st);
     OutArgs B{};
     B.C = P->Cws; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
@@ -873,7 +883,10 @@ static int configure(Plan* P, int64_t max_chunk) {
         return fail(DGT_EUNSUPPORTED, "inner channel count " + std::to_string(I.iM) + " too large for shared memory");
     P->NT = nt;
     P->smemB = smemB(nt);
-    CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+    CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+    P->zct = (P->allu && I.d == 180 && !std::getenv("NSDGT_ZAK_RT")) ? 180 : 0;
+    if (P->zct)
+        CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T, 180>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
     // out_f4096: 2 CTAs per SM for c128 (128 registers, measured faster than 3 CTAs at 80
     // registers with spills), 3 for c64

@@ -211,6 +211,72 @@ __device__ cx<T>* fft_smem(cx<T>* a, cx<T>* b, const Radices& rd, int nseq, int 
     return a;
 }
 
+// ---- compile-time variants (lengths the planner meets on hot lattices, e.g. d = 180 of
+// config 4): every index divides by a constant, composite radices run as register DFTs ----
+
+// Length-(P Q) DFT in registers, natural order in and out (Cooley-Tukey, n = Q n1 + n2,
+// k = k1 + P k2); W_{PQ}^e = tw[e * tws] from the length-N table.
+template <typename T, int P, int Q>
+__device__ __forceinline__ void dft_pq(cx<T>* v, const cx<T>* __restrict__ tw, int tws) {
+    cx<T> a[P * Q];
+#pragma unroll
+    for (int n2 = 0; n2 < Q; ++n2) {
+        cx<T> t[P];
+#pragma unroll
+        for (int n1 = 0; n1 < P; ++n1) t[n1] = v[Q * n1 + n2];
+        dft_fixed<T, P>(t);
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) a[n2 * P + k1] = (n2 && k1) ? cmul(t[k1], tw[n2 * k1 * tws]) : t[k1];
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+        cx<T> t[Q];
+#pragma unroll
+        for (int n2 = 0; n2 < Q; ++n2) t[n2] = a[n2 * P + k1];
+        dft_fixed<T, Q>(t);
+#pragma unroll
+        for (int k2 = 0; k2 < Q; ++k2) v[k1 + P * k2] = t[k2];
+    }
+}
+
+// One Stockham pass, radix R = P Q (Q = 1: a fixed radix), NS = product of earlier radices.
+template <typename T, int N, int P, int Q, int NS>
+__device__ __forceinline__ void stage_ct(const cx<T>* __restrict__ in, cx<T>* __restrict__ out, int nseq,
+                                         const cx<T>* __restrict__ tw) {
+    constexpr int R = P * Q, nb = N / R, tstep = N / (NS * R);
+    for (int t = threadIdx.x; t < nb * nseq; t += blockDim.x) {
+        const int seq = t / nb, j = t - seq * nb;
+        const int k = j % NS;
+        const cx<T>* src = in + seq * N;
+        cx<T>* dst = out + seq * N;
+        cx<T> v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = src[j + r * nb];
+        if (NS > 1) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r * k * tstep]);
+        }
+        if constexpr (Q > 1) dft_pq<T, P, Q>(v, tw, N / R);
+        else dft_fixed<T, P>(v);
+        const int base = (j / NS) * NS * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[base + r * NS] = v[r];
+    }
+}
+
+// DFT of nseq sequences of compile-time length N (stride N); returns the result buffer.
+// N = 180: radix 15 (3 x 5) then 12 (4 x 3) -- odd first-pass write stride, so the
+// 16-byte stores of a quarter warp hit distinct banks.
+template <typename T, int N>
+__device__ cx<T>* fft_ct(cx<T>* a, cx<T>* b, int nseq, const cx<T>* __restrict__ tw) {
+    static_assert(N == 180, "fft_ct: add a radix plan for this length");
+    stage_ct<T, 180, 3, 5, 1>(a, b, nseq, tw);
+    __syncthreads();
+    stage_ct<T, 180, 4, 3, 15>(b, a, nseq, tw);
+    __syncthreads();
+    return a;
+}
+
 // Host: split n into radices (16, 8, 4, 2 for powers of two; then 5, 3; then primes).
 inline Radices make_radices(int n) {
     Radices rd{};
