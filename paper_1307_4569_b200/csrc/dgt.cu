@@ -204,8 +204,7 @@ struct ZakArgs {
     const void* tw;     // twiddles of length d
 };
 
-// DCT > 0: compile-time inner length d = DCT (all-u mode only), DFTs by fft_ct
-template <typename T, int DCT>
+template <typename T>
 __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
@@ -227,7 +226,7 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
     // 1. gather f~(x(r,k,l,s)), x = r + c((k q + p l + s p q) mod (L/c)), rr fastest.
     //    32-bit index arithmetic within a signal (the host checks L < 2^31).
     const int ng = nr * (int)p * (int)d;
-    const int di = DCT ? DCT : (int)d, pi = (int)p, qi = (int)q, ci = (int)c, Lci = (int)Lc;
+    const int di = (int)d, pi = (int)p, qi = (int)q, ci = (int)c, Lci = (int)Lc;
     const int base_kq = pi * l;                     // p l
     const T* fr = (const T*)A.f + w * L;            // real input
     const C* fc = (const C*)A.f + w * L;
@@ -252,9 +251,7 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
         // q RB d; Phi lives in the first nr d of one of them.
         C* R1 = bufA;
         C* R2 = bufA + (size_t)qi * RB * d;
-        C* phi;
-        if constexpr (DCT > 0) phi = fft_ct<T, DCT>(R1, R2, nr, tw);
-        else phi = fft_smem<T>(R1, R2, A.rd, nr, di, tw);
+        C* phi = fft_smem<T>(R1, R2, A.rd, nr, di, tw);
         C* Yb = (phi == R1) ? R2 : R1;
         const C* __restrict__ G = (const C*)A.G;
         const int nrd = nr * di;
@@ -264,9 +261,7 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
             Yb[i] = cmul(phi[rem], G[(((int)r0 + rr) * qi + u) * di + nu]);
         }
         __syncthreads();
-        C* Y;
-        if constexpr (DCT > 0) Y = fft_ct<T, DCT>(Yb, phi, qi * nr, tw);
-        else Y = fft_smem<T>(Yb, phi, A.rd, qi * nr, di, tw);
+        C* Y = fft_smem<T>(Yb, phi, A.rd, qi * nr, di, tw);
         C* Cw = (C*)A.C + w * A.iM * q * d;
         const int jbase = (int)(r0 + c * ((l * p) % q));
         for (int i = threadIdx.x; i < qi * nrd; i += blockDim.x) {
@@ -280,7 +275,6 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
         }
         return;
     }
-    if constexpr (DCT > 0) return;   // compile-time lengths run the all-u mode only
     // 2. DFT_d over s for nr*p sequences
     C* phi = fft_smem<T>(bufA, bufB, A.rd, nr * (int)p, (int)d, tw);
     C* free0 = (phi == bufA) ? bufB : bufA;
@@ -315,6 +309,94 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
             Cw[((jbase + rr) * qi + kappa) * di + np] = Y[rr * di + tau];
         }
         __syncthreads();
+    }
+}
+
+// All-u Zak kernel with compile-time inner length D, q = Q and RBC columns per CTA (config 4:
+// D = 180, Q = 4, RBC = 4 for c128).  Same phases as zak_kernel's all-u mode (gather with
+// the chirp on load, DFT_D of the RBC columns, the Q RBC window products, one DFT_D of Q RBC
+// sequences, scatter), but every index divides by a constant, each thread issues all its
+// global loads of a phase before using them, and p = 1 makes the gather index
+// z = l + Q s < L/c (no reduction).
+template <typename T, int D, int Q, int RBC>
+__global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using C = cx<T>;
+    constexpr int NT = 256, NG = (RBC * D + NT - 1) / NT, NP = (Q * RBC * D + NT - 1) / NT;
+    const int c = (int)A.c;
+    const int nrb = c / RBC;
+    const int rblk = blockIdx.x % nrb, l = blockIdx.x / nrb;
+    const int64_t w = blockIdx.y;
+    const int r0 = rblk * RBC;
+    C* R1 = (C*)smem_raw;
+    C* R2 = R1 + Q * RBC * D;
+    const C* __restrict__ tw = (const C*)A.tw;
+    const C* __restrict__ chirp = (const C*)A.chirp;
+    const int tid = threadIdx.x;
+    {
+        // gather f~(r0 + rr + c (l + Q s)), rr fastest (RBC consecutive residues per row s)
+        const C* fc = (const C*)A.f + w * A.L;
+        const T* fr = (const T*)A.f + w * A.L;
+        C v[NG];
+#pragma unroll
+        for (int it = 0; it < NG; ++it) {
+            const int i = tid + it * NT;
+            if (i < RBC * D) {
+                const int rr = i % RBC, s = i / RBC;
+                const int x = r0 + rr + c * (l + Q * s);
+                v[it] = A.real_in ? mk<T>(fr[x], T(0)) : fc[x];
+            }
+        }
+        if (chirp) {
+#pragma unroll
+            for (int it = 0; it < NG; ++it) {
+                const int i = tid + it * NT;
+                if (i < RBC * D) {
+                    const int rr = i % RBC, s = i / RBC;
+                    v[it] = cmul(v[it], __ldg(chirp + r0 + rr + c * (l + Q * s)));
+                }
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < NG; ++it) {
+            const int i = tid + it * NT;
+            if (i < RBC * D) R1[(i % RBC) * D + i / RBC] = v[it];
+        }
+    }
+    __syncthreads();
+    C* phi = fft_ct<T, D>(R1, R2, RBC, tw);     // Phi in R1[0, RBC D)
+    {
+        const C* __restrict__ G = (const C*)A.G;
+        C gv[NP];
+#pragma unroll
+        for (int it = 0; it < NP; ++it) {
+            const int i = tid + it * NT;
+            if (i < Q * RBC * D) {
+                const int u = i / (RBC * D), rem = i % (RBC * D);
+                gv[it] = __ldg(G + ((r0 + rem / D) * Q + u) * D + rem % D);
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < NP; ++it) {
+            const int i = tid + it * NT;
+            if (i < Q * RBC * D) R2[i] = cmul(phi[i % (RBC * D)], gv[it]);
+        }
+    }
+    __syncthreads();
+    C* Y = fft_ct<T, D>(R2, R1, Q * RBC, tw);    // result in R2
+    C* Cw = (C*)A.C + w * A.iM * Q * D;
+    const int jbase = r0 + c * (l % Q);
+#pragma unroll
+    for (int it = 0; it < NP; ++it) {
+        const int i = tid + it * NT;
+        if (i < Q * RBC * D) {
+            const int u = i / (RBC * D), rem = i % (RBC * D);
+            const int rr = rem / D, np = rem % D;
+            const int kappa = (l - u + Q) % Q;
+            int tau = D - np - (l < u ? 1 : 0);    // (-n' - [l < u]) mod D
+            if (tau >= D) tau -= D;
+            Cw[((jbase + rr) * Q + kappa) * D + np] = Y[(u * RBC + rr) * D + tau];
+        }
     }
 }
 
@@ -804,10 +886,12 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = P->allu;
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
-    if (P->zct == 180)
-        zak_kernel<T, 180><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+    if (P->zct == 180 && sizeof(C) == 16)
+        zak_ct_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+    else if (P->zct == 180)
+        zak_ct_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     else
-        zak_kernel<T, 0><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+        zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     prof_close(P, ph, PK_ZAK, by_in, fl_zak, st);
     OutArgs B{};
     B.C = P->Cws; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
@@ -883,10 +967,14 @@ static int configure(Plan* P, int64_t max_chunk) {
         return fail(DGT_EUNSUPPORTED, "inner channel count " + std::to_string(I.iM) + " too large for shared memory");
     P->NT = nt;
     P->smemB = smemB(nt);
-    CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
-    P->zct = (P->allu && I.d == 180 && !std::getenv("NSDGT_ZAK_RT")) ? 180 : 0;
-    if (P->zct)
-        CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T, 180>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+    CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+    // compile-time Zak kernel: d = 180, q = 4, p = 1, RB = 64 / e columns dividing c
+    P->zct = (P->allu && I.d == 180 && I.q == 4 && I.c % P->RB == 0 && P->RB == (int)(64 / e) &&
+              !std::getenv("NSDGT_ZAK_RT")) ? 180 : 0;
+    if (P->zct) {
+        CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+        CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+    }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
     // out_f4096: 2 CTAs per SM for c128 (128 registers, measured faster than 3 CTAs at 80
     // registers with spills), 3 for c64

@@ -189,6 +189,21 @@ def test_fbranch_out4096_kernel(torch_cuda, nsdgt, oracle_mod, dtype, monkeypatc
     assert rel(c, cg) <= TOL[dtype]
 
 
+def test_config4_lattice_c64_sampled(torch_cuda, nsdgt, oracle_mod):
+    """Config 4's lattice in complex64 (the d = 180 Zak kernel's 8-column variant and
+    out_f4096 in fp32): sampled columns of two signals against the oracle."""
+    torch = torch_cuda
+    wl = CONFIGS[3]
+    g = window(wl).astype(np.complex64)
+    f = batch(wl, 0, 2).astype(np.complex64)
+    plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c64")
+    c = plan.execute(torch.from_numpy(f).cuda())
+    cols = np.sort(np.random.default_rng(44).choice(wl.N, 24, replace=False))
+    ref = oracle_mod.dgt(f, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols)
+    got = c[:, :, torch.from_numpy(cols).cuda()].cpu().numpy()
+    assert rel(got, ref) <= TOL["c64"]
+
+
 def test_chunking_ragged_and_host_path(torch_cuda, nsdgt):
     """Ragged chunks (W not a multiple of the chunk), W = 0, and the host end-to-end path
     give bitwise the same result as one device execute."""
