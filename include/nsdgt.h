@@ -122,8 +122,9 @@ int dgt_destroy(dgt_plan_t plan);
 /* Copy the plan's planner record (with chunk, workspace and kernel path filled in). */
 int dgt_plan_query(dgt_plan_t plan, dgt_lattice_info* info);
 
-/* Number of kernel launches one dgt_execute of W signals issues (cuFFT launches counted
- * as one per call).  Used by bench.py for its gpu_launches claim. */
+/* Number of this library's own kernel launches (and memsets) one dgt_execute of W signals
+ * issues; the frequency-shear path's cuFFT calls are library launches and not counted.
+ * Used by bench.py for its gpu_launches claim. */
 int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W);
 
 /* Per-kernel profiling (used by bench.py for its roofline line).  After dgt_profile_begin,
