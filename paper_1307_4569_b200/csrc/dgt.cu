@@ -720,8 +720,9 @@ struct Plan {
     size_t pool_used = 0;
 };
 
-enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_COUNT = 4 };
-static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast"};
+enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_COUNT = 6 };
+static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
+                                           "zak_ct_d180", "out_f4096"};
 
 static cudaEvent_t prof_event(Plan* P) {
     if (P->pool_used == P->pool.size()) {
@@ -918,7 +919,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
         zak_ct_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     else
         zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
-    prof_close(P, ph, PK_ZAK, by_in, fl_zak, st);
+    prof_close(P, ph, P->zct ? PK_ZAKCT : PK_ZAK, by_in, fl_zak, st);
     OutArgs B{};
     B.C = P->Cws; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
     B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
@@ -946,7 +947,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
         out_f4096_kernel<T, 2><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
     else
         out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
-    prof_close(P, ph, PK_OUT, by_out, fl_out, st);
+    prof_close(P, ph, P->outk ? PK_OUTF : PK_OUT, by_out, fl_out, st);
     CUDA_TRY(cudaGetLastError());
     return DGT_OK;
 }
