@@ -9,7 +9,11 @@ the DESIGN.md readings Z1 (0-based window shift) and Z2 (frequency index from th
 lowest non-negative frequency).  See ``dgt_oracle.c`` for the two evaluations
 (O1 literal sum, O2 regrouped sum).  Pins: ``tests/test_oracle_pins.py``.
 
-Parity pinned for: ``dgt`` (both variants).  Nothing here is "parity unpinned".
+``idgt`` is the synthesis operator (the inverse DGT with a dual window, the inversion
+formula of PAPER.md:171-175), the adjoint of Eq. (DGT).
+
+Parity pinned for: ``dgt`` and ``idgt`` (both variants each).  Nothing here is "parity
+unpinned".
 """
 from __future__ import annotations
 
@@ -45,6 +49,10 @@ def _load():
         for name in ("oracle_dgt_literal", "oracle_dgt_regrouped"):
             fn = getattr(lib, name)
             fn.argtypes = [P, P, I, I, I, I, I, I, P, I, P, ctypes.c_int]
+            fn.restype = ctypes.c_int
+        for name in ("oracle_idgt_literal", "oracle_idgt_regrouped"):
+            fn = getattr(lib, name)
+            fn.argtypes = [P, P, I, I, I, I, I, I, P, ctypes.c_int]
             fn.restype = ctypes.c_int
         lib.oracle_threads.restype = ctypes.c_int
         _lib = lib
@@ -89,3 +97,31 @@ def dgt(f, g, a: int, M: int, lam1: int, lam2: int, cols=None, variant: str = "a
         raise ValueError(f"oracle rejected arguments (status {rc}): L={L} a={a} M={M} "
                          f"lambda={lam1}/{lam2}")
     return c[0] if squeeze else c
+
+
+def idgt(c, gamma, a: int, M: int, lam1: int, lam2: int, variant: str = "auto",
+         nthreads: int = 0) -> np.ndarray:
+    """f[w, l] = sum_{m,n} c_w(m,n) gamma((l - a n) mod L) exp(2 pi i l (m + w(n)) / M), fp64.
+
+    ``c``: (M, N) or (W, M, N); ``gamma``: (L,) synthesis window (the canonical dual of the
+    analysis window inverts Eq. (DGT)).  ``variant``: "literal" (S1), "regrouped" (S2) or
+    "auto".  Returns complex128 (L,) or (W, L).
+    """
+    lib = _load()
+    c = np.asarray(c)
+    squeeze = c.ndim == 2
+    c3 = np.ascontiguousarray(c[None] if squeeze else c, dtype=np.complex128)
+    g2 = np.ascontiguousarray(np.asarray(gamma), dtype=np.complex128)
+    L = g2.shape[0]
+    W, Mc, N = c3.shape
+    if Mc != M or a <= 0 or N * a != L:
+        raise ValueError("c must have shape (W, M, L/a)")
+    f = np.zeros((W, L), dtype=np.complex128)
+    if variant == "auto":
+        variant = "literal" if L * M * N <= 1 << 22 else "regrouped"
+    fn = lib.oracle_idgt_literal if variant == "literal" else lib.oracle_idgt_regrouped
+    rc = fn(c3.ctypes.data, g2.ctypes.data, L, a, M, lam1, lam2, W, f.ctypes.data, int(nthreads))
+    if rc != 0:
+        raise ValueError(f"oracle rejected arguments (status {rc}): L={L} a={a} M={M} "
+                         f"lambda={lam1}/{lam2}")
+    return f[0] if squeeze else f

@@ -207,3 +207,123 @@ int oracle_dgt_regrouped(const double* f, const double* g, int64_t L, int64_t a,
     free(om);
     return 0;
 }
+
+/*
+ * Synthesis (the inverse DGT with a dual window): the inversion formula
+ * f = sum c(m,n) S^{-1} pi(x,omega) g of PAPER.md:171-175 (Sec. 2.1) with the canonical
+ * dual gamma = S^{-1} g, indexed as Eq. (DGT) indexes the coefficients:
+ *
+ *   f_w(l) = sum_{n<N} sum_{m<M} c_w(m,n) gamma((l - a n) mod L) exp(+2 pi i l (m + w(n)) / M).
+ *
+ * This is the adjoint of Eq. (DGT) with window gamma.  gamma is an input (any window; pass
+ * the canonical dual to invert).  Layout: c is W x M x N (n fastest), f is W x L, all
+ * interleaved complex doubles.  Phases reduced exactly as in O1 (conjugated omega).
+ *   S1 literal  : the double sum as written, per l.
+ *   S2 regrouped: l = j + t M:  H_n(j) = sum_m c(m,n) exp(2 pi i j (m + w(n)) / M),
+ *                 f(j + t M) = sum_n gamma(j + t M - a n) exp(2 pi i t w'(n) / lambda2) H_n(j),
+ *                 w' = n lambda1 mod lambda2  (exp(2 pi i t M (m + w)/M) = exp(2 pi i t w)).
+ * OpenMP over (w, l) (S1) or (w, j) (S2); every output is written by one thread.
+ */
+int oracle_idgt_literal(const double* c, const double* g, int64_t L, int64_t a, int64_t M,
+                        int64_t l1, int64_t l2, int64_t W, double* f, int nthreads) {
+    int rc = check_args(L, a, M, l1, l2, W);
+    if (rc) return rc;
+    const int64_t N = L / a;
+    const int64_t K = l2 * M;
+    double* om = make_omega(K);
+    set_threads(nthreads);
+    const int64_t total = W * L;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t job = 0; job < total; ++job) {
+        const int64_t w = job / L, l = job % L;
+        const double* cw = c + 2 * w * M * N;
+        ld sr = 0.0L, si = 0.0L;
+        for (int64_t n = 0; n < N; ++n) {
+            const int64_t gi = ((l - a * n) % L + L) % L;
+            const double gr = g[2 * gi], gim = g[2 * gi + 1];
+            const int64_t wp = (n * l1) % l2;
+            double br = 0.0, bi = 0.0;
+            for (int64_t m = 0; m < M; ++m) {
+                /* exp(+2 pi i l (m lambda2 + w') / (lambda2 M)) = conj(omega[k]) */
+                const int64_t k = ((l % K) * ((m * l2 + wp) % K)) % K;
+                const double er = om[2 * k], ei = -om[2 * k + 1];
+                const double cr = cw[2 * (m * N + n)], ci = cw[2 * (m * N + n) + 1];
+                /* c * gamma * e */
+                const double pr = cr * gr - ci * gim, pi = cr * gim + ci * gr;
+                br += pr * er - pi * ei;
+                bi += pr * ei + pi * er;
+            }
+            sr += br;
+            si += bi;
+        }
+        f[2 * (w * L + l)] = (double)sr;
+        f[2 * (w * L + l) + 1] = (double)si;
+    }
+    free(om);
+    return 0;
+}
+
+int oracle_idgt_regrouped(const double* c, const double* g, int64_t L, int64_t a, int64_t M,
+                          int64_t l1, int64_t l2, int64_t W, double* f, int nthreads) {
+    int rc = check_args(L, a, M, l1, l2, W);
+    if (rc) return rc;
+    const int64_t N = L / a, b = L / M;
+    const int64_t K = l2 * M;
+    double* om = make_omega(K);
+    double* zeta = (double*)malloc(sizeof(double) * 2 * (size_t)l2); /* exp(+2 pi i k / lambda2) */
+    for (int64_t k = 0; k < l2; ++k) {
+        ld th = 2.0L * ORACLE_PI * (ld)k / (ld)l2;
+        zeta[2 * k] = (double)cosl(th);
+        zeta[2 * k + 1] = (double)sinl(th);
+    }
+    set_threads(nthreads);
+    const int64_t total = W * M;
+#pragma omp parallel
+    {
+        double* H = (double*)malloc(sizeof(double) * 2 * (size_t)N);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t job = 0; job < total; ++job) {
+            const int64_t w = job / M, j = job % M;
+            const double* cw = c + 2 * w * M * N;
+            for (int64_t n = 0; n < N; ++n) {
+                const int64_t wp = (n * l1) % l2;
+                ld sr = 0.0L, si = 0.0L;
+                double br = 0.0, bi = 0.0;
+                for (int64_t m = 0; m < M; ++m) {
+                    const int64_t k = (j * ((m * l2 + wp) % K)) % K;
+                    const double er = om[2 * k], ei = -om[2 * k + 1];
+                    const double cr = cw[2 * (m * N + n)], ci = cw[2 * (m * N + n) + 1];
+                    br += cr * er - ci * ei;
+                    bi += cr * ei + ci * er;
+                    if ((m & 63) == 63) { sr += br; si += bi; br = bi = 0.0; }
+                }
+                sr += br; si += bi;
+                H[2 * n] = (double)sr;
+                H[2 * n + 1] = (double)si;
+            }
+            for (int64_t t = 0; t < b; ++t) {
+                const int64_t l = j + t * M;
+                ld sr = 0.0L, si = 0.0L;
+                double br = 0.0, bi = 0.0;
+                for (int64_t n = 0; n < N; ++n) {
+                    const int64_t gi = ((l - a * n) % L + L) % L;
+                    const double gr = g[2 * gi], gim = g[2 * gi + 1];
+                    const int64_t zk = (((n * l1) % l2) * t) % l2;
+                    const double zr = zeta[2 * zk], zi = zeta[2 * zk + 1];
+                    /* gamma * zeta * H(n) */
+                    const double qr = gr * zr - gim * zi, qi = gr * zi + gim * zr;
+                    br += qr * H[2 * n] - qi * H[2 * n + 1];
+                    bi += qr * H[2 * n + 1] + qi * H[2 * n];
+                    if ((n & 63) == 63) { sr += br; si += bi; br = bi = 0.0; }
+                }
+                sr += br; si += bi;
+                f[2 * (w * L + l)] = (double)sr;
+                f[2 * (w * L + l) + 1] = (double)si;
+            }
+        }
+        free(H);
+    }
+    free(zeta);
+    free(om);
+    return 0;
+}

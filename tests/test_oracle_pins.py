@@ -196,3 +196,55 @@ def test_config1_window_properties():
     assert abs(np.linalg.norm(g) - 1) < 1e-14
     assert np.allclose(g[1:], g[1:][::-1], rtol=0, atol=1e-15)
     assert math.isclose(g[0], g.max())
+
+
+# ---- synthesis (inverse DGT): oracle.idgt ----
+
+@pytest.mark.parametrize("L,a,M,l1,l2", TINY)
+@pytest.mark.parametrize("variant", ["literal", "regrouped"])
+def test_idgt_dense_atoms(oracle_mod, L, a, M, l1, l2, variant):
+    """S1/S2 against the dense synthesis matrix whose columns are the atoms
+    M_{sn+bk} T_{an} gamma built from the operator definitions."""
+    rng = np.random.default_rng(L + 7 * M + l1)
+    N = L // a
+    c = rng.standard_normal((M, N)) + 1j * rng.standard_normal((M, N))
+    _, gamma = random_pair(L, 31)
+    ref = dense.synthesize(c, gamma, a, M, l1, l2)
+    assert rel(oracle_mod.idgt(c, gamma, a, M, l1, l2, variant=variant), ref) < 1e-12
+
+
+@pytest.mark.parametrize("L,a,M,l1,l2", [(72, 8, 12, 1, 3), (240, 8, 12, 1, 2), (1440, 30, 48, 2, 3),
+                                         (2880, 60, 240, 1, 3)])
+def test_idgt_is_adjoint_of_dgt(oracle_mod, L, a, M, l1, l2):
+    """<dgt(f, g), c> = <f, idgt(c, g)> for random f, c (the synthesis operator is the adjoint
+    of the analysis operator with the same window; dgt is pinned independently above)."""
+    rng = np.random.default_rng(L)
+    f, g = random_pair(L, 33)
+    N = L // a
+    c = rng.standard_normal((M, N)) + 1j * rng.standard_normal((M, N))
+    lhs = np.vdot(c, oracle_mod.dgt(f, g, a, M, l1, l2))          # <dgt f, c> conj-linear in c
+    rhs = np.vdot(oracle_mod.idgt(c, g, a, M, l1, l2), f)         # <f, idgt c>
+    assert abs(lhs - rhs) <= 1e-11 * abs(lhs)
+
+
+@pytest.mark.parametrize("L,a,M,l1,l2", [(36, 6, 6, 1, 2), (72, 8, 12, 1, 3), (240, 8, 12, 1, 2)])
+def test_idgt_perfect_reconstruction(oracle_mod, L, a, M, l1, l2):
+    """idgt(dgt(f, g), S^{-1} g) = f (inversion formula), the dual from the
+    dense frame operator."""
+    g = pgauss(L, a * M / L)
+    gamma = dense.canonical_dual(g, a, M, l1, l2)
+    f, _ = random_pair(L, 34)
+    f_rec = oracle_mod.idgt(oracle_mod.dgt(f, g, a, M, l1, l2), gamma, a, M, l1, l2)
+    assert rel(f_rec, f.astype(complex)) < 1e-11
+
+
+@pytest.mark.parametrize("L,a,M,l1,l2", [(216, 12, 18, 1, 3), (720, 60, 240, 1, 3), (512, 64, 256, 1, 2)])
+def test_idgt_literal_equals_regrouped_batch(oracle_mod, L, a, M, l1, l2):
+    rng = np.random.default_rng(5)
+    N = L // a
+    c = rng.standard_normal((2, M, N)) + 1j * rng.standard_normal((2, M, N))
+    _, gamma = random_pair(L, 35)
+    f1 = oracle_mod.idgt(c, gamma, a, M, l1, l2, variant="literal")
+    f2 = oracle_mod.idgt(c, gamma, a, M, l1, l2, variant="regrouped")
+    assert f1.shape == (2, L) and rel(f1, f2) < 1e-13
+    assert rel(oracle_mod.idgt(c[1], gamma, a, M, l1, l2), f2[1]) < 1e-13
