@@ -110,6 +110,18 @@ int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t lambda1, 
  * W = 0 is a no-op.  Errors: DGT_EINVAL (null/aliasing), DGT_ECUDA, DGT_ECUFFT. */
 int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_stream);
 
+/* Synthesis (inverse DGT) with the plan's window as the synthesis window gamma
+ * (the inversion formula of PAPER.md:171-175, Sec. 2.1):
+ *   f_w(l) = sum_{n<N} sum_{m<M} c_w(m,n) gamma((l - a n) mod L) exp(+2 pi i l (m + w(n)) / M),
+ * i.e. the adjoint of dgt_execute.  A plan built with the canonical dual window S^{-1} g
+ * inverts the DGT of a plan built with g.  c: device, W x M x N complex (n fastest), read
+ * only.  f: device, W x L complex of the plan's dtype (always complex, also for
+ * DGT_REAL_INPUT plans), fully overwritten.  Asynchronous and stream-ordered; the first call
+ * allocates the plan's synthesis workspace (kept until dgt_destroy).  Runs the generic
+ * (adjoint) kernels for every lattice.  W = 0 is a no-op.
+ * Errors: DGT_EINVAL (null/aliasing, W < 0), DGT_ECUDA, DGT_ECUFFT, DGT_ENOMEM. */
+int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void* cuda_stream);
+
 /* End-to-end variant with HOST buffers: copies f (host, W x L) to the device, runs the
  * transform and copies c (host, W x M x N) back, chunk by chunk with the copies overlapped
  * on two extra streams.  Returns after c is complete on the host (synchronous).  Staging

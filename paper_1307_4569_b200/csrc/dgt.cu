@@ -668,6 +668,175 @@ __global__ void __launch_bounds__(256, MINB) out_f4096_kernel(OutArgs A) {
 constexpr size_t kOutF4096Elems = 16 * 272;
 
 // ---------------------------------------------------------------------------------
+// synthesis (the inverse DGT with the plan's window as the synthesis window gamma; SURVEY
+// NEXT-1): f = sum_{m,n} c(m,n) M_{b(m+w(n))} T_{an} gamma, the inversion formula of
+// PAPER.md:171-175 (pass the canonical dual S^{-1} g to invert).  It is the adjoint of the
+// forward pipeline, so the kernels run the forward steps backwards with every linear map
+// replaced by its adjoint: permutations by their inverses, multipliers by their conjugates,
+// the forward DFTs by unnormalised inverse DFTs, computed as conj(DFT(conj(.))) on the same
+// Stockham engine (the conjugations are folded into the loads and stores).
+// ---------------------------------------------------------------------------------
+
+// Adjoint of out_kernel: c[w][M][N] -> C[w][j][kappa][n'].  Same CTA tiling as out_kernel.
+//   T-branch: X'(m', n) = conj(E(n)) c[(m' - rot(n)) mod M][n];  F-branch: X'(kc, m) =
+//   conj(E(k,m)) c[kt][mt] (the Alg. 1 remap read backwards);  then C'(j, n) = sum_m' X'(m', n)
+//   exp(+2 pi i j m' / iM).
+template <typename T>
+__global__ void __launch_bounds__(256) out_adj_kernel(OutArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using C = cx<T>;
+    const int64_t iM = A.iM, iN = A.iN, q = A.q, d = A.d;
+    const int NT = A.NT;
+    const int iMi = (int)iM, qi = (int)q, di = (int)d;
+    int64_t nb, ns;
+    int nt;
+    if (A.grouped) {
+        const int kap = (int)(blockIdx.x % q), blk = (int)(blockIdx.x / q);
+        nb = kap + q * (int64_t)blk * NT;
+        ns = q;
+        nt = (int)((d - (int64_t)blk * NT) < NT ? (d - (int64_t)blk * NT) : NT);
+    } else {
+        nb = (int64_t)blockIdx.x * NT;
+        ns = 1;
+        nt = (int)((iN - nb) < NT ? (iN - nb) : NT);
+    }
+    const int64_t w = blockIdx.y;
+    C* bufA = (C*)smem_raw;
+    C* bufB = bufA + (size_t)NT * iM;
+    const C* cin = (const C*)A.out + w * A.M * A.N;   // the coefficients (input here)
+    // bufA = conj(X'), the input of the forward engine
+    if (A.branch != DGT_BRANCH_FREQ) {
+        const C* E = (const C*)A.E;
+        const int Mi = (int)A.M, Ni = (int)A.N;
+        for (int i = threadIdx.x; i < nt * iMi; i += blockDim.x) {
+            const int cl = i % nt, mo = i / nt;
+            const int n = (int)nb + cl;
+            int m = mo + A.rot[n];
+            if (m >= Mi) m -= Mi;
+            // c[mo][n] = E(n) X(m, n)  =>  conj(X'(m, n)) = E(n) conj(c[mo][n])
+            const C v = cin[(size_t)mo * Ni + n];
+            bufA[cl * iMi + m] = cmul(E[n], mk<T>(v.x, -v.y));
+        }
+    } else {
+        const unsigned int Nn = (unsigned int)A.N;
+        for (int cl = 0; cl < nt; ++cl) {
+            const FbCol cc = fb_col(A, (unsigned long long)(nb + ns * cl));
+            const unsigned int kc0 = threadIdx.x;   // blockDim.x == 256
+            const int cnt = (iMi - (int)kc0 + 255) / 256;
+            if (cnt <= 0) continue;
+            FbIter<C> it = fb_iter<C>(A, cc, kc0 ? (unsigned long long)A.Nr - kc0 : 0ull);
+            for (int i = 0; i < cnt; ++i) {
+                if (i == 1 && kc0 == 0) it = fb_iter<C>(A, cc, (unsigned long long)A.Nr - 256u);
+                else if (i > 0) fb_step(A, it);
+                const unsigned int twoN = 2 * Nn;
+                C ph;
+                if (A.C3) {
+                    const unsigned int s2 = bmod((unsigned long long)it.sq * it.sq, twoN, A.inv2N);
+                    const unsigned int t1 = bmod((unsigned long long)A.C3 * s2, twoN, A.inv2N);
+                    ph = __ldg((const C*)A.ptab + submod(t1, it.t2, twoN));
+                } else {
+                    ph = it.ph;
+                }
+                const unsigned int mt = it.sq >= Nn ? it.sq - Nn : it.sq;
+                const unsigned int bu = (unsigned int)A.b;
+                unsigned int kt = __umulhi(it.xx, A.invb);
+                unsigned int r = it.xx - kt * bu;
+                if (r >= bu) { r -= bu; ++kt; }
+                if (r >= bu) ++kt;
+                const C v = cin[(size_t)kt * Nn + mt];
+                bufA[cl * iMi + kc0 + 256 * i] = cmul(ph, mk<T>(v.x, -v.y));
+            }
+        }
+    }
+    __syncthreads();
+    C* X = fft_smem<T>(bufA, bufB, A.rd, nt, iMi, (const C*)A.tw);
+    // C'(j, n) = conj(X(j)), stored at [j][n mod q][n div q]
+    C* Cw = (C*)A.C + w * iM * iN;
+    for (int i = threadIdx.x; i < nt * iMi; i += blockDim.x) {
+        const int cl = i % nt, j = i / nt;
+        const int n = (int)(nb + ns * cl);
+        const int nq = n / qi;
+        const C v = X[cl * iMi + j];
+        Cw[(j * qi + (n - nq * qi)) * di + nq] = mk<T>(v.x, -v.y);
+    }
+}
+
+// Adjoint of zak_kernel: C[w][j][kappa][n'] -> f~[w][x].  Same CTA tiling (signal, residue
+// block, l).  Per u: gather T'(tau) (the scatter read backwards), adjoint DFT_d over tau,
+// accumulate Phi'(k; nu) += Y'_u(nu) conj(G(k, u; nu)); then the adjoint DFT_d over nu and the
+// write through the (bijective, gcd(p, q) = 1) Zak index map with conj(chirp).  Buffers: the
+// conjugated accumulator acc (RB p d), scratch B (RB p d >= RB d), Y (RB d).
+template <typename T>
+__global__ void __launch_bounds__(256) zak_adj_kernel(ZakArgs A, void* fout) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using C = cx<T>;
+    const int64_t d = A.d, p = A.p, q = A.q, c = A.c, L = A.L;
+    const int RB = A.RB;
+    const int nrb = (int)((c + RB - 1) / RB);
+    const int rblk = blockIdx.x % nrb;
+    const int l = blockIdx.x / nrb;
+    const int64_t w = blockIdx.y;
+    const int64_t r0 = (int64_t)rblk * RB;
+    const int nr = (int)((c - r0) < RB ? (c - r0) : RB);
+    C* acc = (C*)smem_raw;                  // RB*p*d: conj(Phi')
+    C* bufB = acc + (size_t)RB * p * d;     // RB*p*d
+    C* bufY = bufB + (size_t)RB * p * d;    // RB*d
+    const C* __restrict__ tw = (const C*)A.tw;
+    const C* __restrict__ G = (const C*)A.G;
+    const int di = (int)d, pi = (int)p, qi = (int)q, ci = (int)c, Lci = (int)(L / c);
+    const C* Cw = (const C*)A.C + w * A.iM * q * d;
+    const int jbase = (int)(r0 + c * ((l * p) % q));
+    for (int u = 0; u < qi; ++u) {
+        const int kappa = ((l - u) % qi + qi) % qi;
+        const int off = (l < u) ? 1 : 0;
+        // gather conj(T'(tau)), tau = (-n' - off) mod d
+        for (int i = threadIdx.x; i < nr * di; i += blockDim.x) {
+            const int rr = i / di, np = i - rr * di;
+            int tau = di - np - off;
+            if (tau >= di) tau -= di;
+            if (tau < 0) tau += di;
+            const C v = Cw[((jbase + rr) * qi + kappa) * di + np];
+            bufB[rr * di + tau] = mk<T>(v.x, -v.y);
+        }
+        __syncthreads();
+        const C* Y = fft_smem<T>(bufB, bufY, A.rd, nr, di, tw);   // Y = conj(Y'_u)
+        // conj(Phi'(k; nu)) += Y(nu) G(k, u; nu)
+        for (int i = threadIdx.x; i < nr * pi * di; i += blockDim.x) {
+            const int rr = i / (pi * di), rem = i - rr * pi * di;
+            const int k = rem / di, nu = rem - k * di;
+            const C t = cmul(Y[rr * di + nu], G[(((r0 + rr) * q + u) * p + k) * d + nu]);
+            acc[i] = u ? acc[i] + t : t;
+        }
+        __syncthreads();
+    }
+    // f~'(s) = conj(DFT(conj(Phi')))(s) = conj(R(s))
+    const C* R = fft_smem<T>(acc, bufB, A.rd, nr * pi, di, tw);
+    const C* __restrict__ chirp = (const C*)A.chirp;
+    C* fo = (C*)fout + w * L;
+    const int base_kq = pi * l;
+    for (int i = threadIdx.x; i < nr * pi * di; i += blockDim.x) {
+        const int rr = i % nr;
+        const int ks = i / nr;   // k*d + s (rr fastest: consecutive residues, coalesced)
+        const int s = ks % di, k = ks / di;
+        int z = k * qi + base_kq + s * pi * qi;
+        z %= Lci;
+        const int x = (int)r0 + rr + ci * z;
+        C v = R[(rr * pi + k) * di + s];
+        if (chirp) v = cmul(v, chirp[x]);
+        fo[x] = mk<T>(v.x, -v.y);   // conj(chirp(x)) f~'(x) = conj(chirp(x) R)
+    }
+}
+
+// out = conj(pre) * in, elementwise over n elements (pre is L-periodic)
+template <typename T>
+__global__ void k_conj_chirp(cx<T>* out, const cx<T>* in, const cx<T>* __restrict__ pre, int64_t L, int64_t total) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const cx<T> p = pre[i % L];
+        out[i] = cmulc(in[i], p);
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // the plan
 // ---------------------------------------------------------------------------------
 
@@ -698,6 +867,12 @@ struct Plan {
     int RB = 1, NT = 1;
     size_t smemA = 0, smemB = 0;
     int allu = 0;            // zak_kernel all-u mode (p = 1)
+    // synthesis (dgt_execute_inverse): chunk, zak_adj_kernel smem, workspace (allocated on
+    // first use: C intermediate + F-branch spectra)
+    int64_t inv_chunk = 1;
+    size_t smemAinv = 0;
+    void* Cinv = nullptr;
+    void* finv = nullptr;
     int zct = 0;             // zak_kernel compile-time inner length (0 = runtime radices)
     int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
     int fast = 0;  // specialised path id (0 = generic)
@@ -720,9 +895,10 @@ struct Plan {
     size_t pool_used = 0;
 };
 
-enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_COUNT = 6 };
+enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_ZAKADJ = 6,
+                PK_OUTADJ = 7, PK_COUNT = 8 };
 static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
-                                           "zak_ct_d180", "out_f4096"};
+                                           "zak_ct_d180", "out_f4096", "zak_adjoint", "out_adjoint"};
 
 static cudaEvent_t prof_event(Plan* P) {
     if (P->pool_used == P->pool.size()) {
@@ -754,7 +930,7 @@ static void prof_close(Plan* P, int h, int kind, double bytes, double flops, cud
 static void free_plan(Plan* P) {
     if (!P) return;
     void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
-                    P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1]};
+                    P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     free_fast(&P->fp);
@@ -1011,9 +1187,14 @@ static int configure(Plan* P, int64_t max_chunk) {
                                   (int)(kOutF4096Elems * e)));
     CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kOutF4096Elems * e)));
+    // synthesis kernels (the adjoints of zak_kernel / out_kernel)
+    P->smemAinv = (size_t)P->RB * (2 * I.p + 1) * I.d * e;
+    CUDA_TRY(cudaFuncSetAttribute(zak_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemAinv));
+    CUDA_TRY(cudaFuncSetAttribute(out_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
     // chunk: intermediate of a chunk stays well inside L2
     const size_t per_sig = (size_t)I.iM * I.iN * e;
     int64_t ch = std::max<int64_t>(1, (int64_t)((size_t)(l2 > 0 ? l2 : (64 << 20)) * 2 / 5 / per_sig));
+    P->inv_chunk = max_chunk > 0 ? max_chunk : ch;
     if (max_chunk > 0) ch = max_chunk;
     P->chunk = ch;
     return DGT_OK;
@@ -1032,6 +1213,82 @@ static int alloc_workspace(Plan* P, int64_t Wc) {
         P->fb = std::max<int64_t>(1, want / Wc) * Wc;
         CUDA_TRY(cudaMalloc(&P->fhat, (size_t)P->fb * per));
         P->ws_bytes += (size_t)P->fb * per;
+    }
+    return DGT_OK;
+}
+
+// Synthesis of Wc signals: c (device, Wc x M x N) -> f (device, Wc x L complex).
+template <typename T>
+static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cudaStream_t st) {
+    using C = cx<T>;
+    const dgt_lattice_info& I = P->info;
+    const double e = (double)sizeof(C), L = (double)I.L, MN = (double)I.M * (double)I.N;
+    OutArgs B{};
+    B.C = P->Cinv; B.out = const_cast<void*>(c); B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
+    B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
+    B.grouped = I.branch == DGT_BRANCH_FREQ ? 1 : 0;
+    B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
+    B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
+    {
+        const int64_t twoN = 2 * I.N;
+        auto nm = [](int64_t v, int64_t m) { return ((v % m) + m) % m; };
+        B.C1 = nm(I.C1, twoN); B.C2 = nm(I.C2, twoN); B.C3 = nm(I.C3, twoN); B.C4 = nm(I.C4, twoN);
+        B.C5 = nm(I.C5, twoN); B.C6 = nm(I.C6, I.L);
+    }
+    B.sar = (((-(I.s1 % I.L)) * (I.a_r % I.L)) % I.L + I.L) % I.L;
+    B.D1 = (unsigned int)((256 * B.C1) % (2 * I.N));
+    B.D5 = (unsigned int)((256 * B.C5) % (2 * I.N));
+    B.DX = (unsigned int)(((__int128)256 * B.sar) % I.L);
+    B.invb = (unsigned int)(0xffffffffull / (unsigned long long)I.b);
+    B.inv2N = ~0ull / (unsigned long long)(2 * I.N);
+    B.invL = ~0ull / (unsigned long long)I.L;
+    const int ntiles = B.grouped ? (int)(I.q * ((I.d + P->NT - 1) / P->NT)) : (int)((I.iN + P->NT - 1) / P->NT);
+    int ph = prof_open(P, st);
+    out_adj_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
+    prof_close(P, ph, PK_OUTADJ, Wc * MN * e, Wc * (4.0 * MN * std::log2((double)I.iM) + 6.0 * MN), st);
+    ZakArgs A{};
+    A.f = nullptr; A.real_in = 0; A.chirp = P->chirp; A.G = P->G; A.C = P->Cinv;
+    A.L = I.L; A.c = I.c; A.d = I.d; A.p = I.p; A.q = I.q; A.iM = I.iM;
+    A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = 0;
+    const int nrb = (int)((I.c + P->RB - 1) / P->RB);
+    const bool freq = I.branch == DGT_BRANCH_FREQ;
+    void* zout = freq ? P->finv : f;
+    const double lg_d = std::log2((double)I.d);
+    ph = prof_open(P, st);
+    zak_adj_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemAinv, st>>>(A, zout);
+    prof_close(P, ph, PK_ZAKADJ, Wc * L * e + L * e, Wc * (8.0 * L * I.q / I.p + 4.0 * L * lg_d + 4.0 * MN * lg_d), st);
+    if (freq) {
+        // adjoint of f^ = fft(pchirp(L, s1) f): unnormalised inverse FFT, then conj(pchirp)
+        ph = prof_open(P, st);
+        cufftHandle h;
+        int rc = get_fft_plan(P, Wc, st, &h);
+        if (rc) return rc;
+        void* dst = P->pre ? P->finv : f;
+        if (P->dtype == DGT_C64)
+            CUFFT_TRY(cufftExecC2C(h, (cufftComplex*)P->finv, (cufftComplex*)dst, CUFFT_INVERSE));
+        else
+            CUFFT_TRY(cufftExecZ2Z(h, (cufftDoubleComplex*)P->finv, (cufftDoubleComplex*)dst, CUFFT_INVERSE));
+        if (P->pre)
+            k_conj_chirp<T><<<grid_for(Wc * I.L), 256, 0, st>>>((C*)f, (const C*)P->finv, (const C*)P->pre, I.L, Wc * I.L);
+        prof_close(P, ph, PK_FRONT, Wc * L * e, Wc * 4.0 * L * std::log2(L), st);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return DGT_OK;
+}
+
+static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStream_t st) {
+    const dgt_lattice_info& I = P->info;
+    if (!P->Cinv) {
+        CUDA_TRY(cudaMalloc(&P->Cinv, (size_t)P->inv_chunk * I.iM * I.iN * P->esz));
+        if (I.branch == DGT_BRANCH_FREQ) CUDA_TRY(cudaMalloc(&P->finv, (size_t)P->inv_chunk * I.L * P->esz));
+    }
+    for (int64_t w0 = 0; w0 < W; w0 += P->inv_chunk) {
+        const int64_t wc = std::min<int64_t>(P->inv_chunk, W - w0);
+        const void* cc = (const char*)c + (size_t)w0 * I.M * I.N * P->esz;
+        void* fc = (char*)f + (size_t)w0 * I.L * P->esz;
+        int rc = P->dtype == DGT_C64 ? launch_inverse_chunk<float>(P, cc, fc, wc, st)
+                                     : launch_inverse_chunk<double>(P, cc, fc, wc, st);
+        if (rc) return rc;
     }
     return DGT_OK;
 }
@@ -1153,6 +1410,19 @@ int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_s
     const size_t fbytes = (size_t)W * P->info.L * ein, cbytes = (size_t)W * P->info.M * P->info.N * P->esz;
     if (fb < cb + cbytes && cb < fb + fbytes) return fail(DGT_EINVAL, "f and c alias");
     return execute(P, f, c, W, (cudaStream_t)cuda_stream);
+}
+
+int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void* cuda_stream) {
+    Plan* P = (Plan*)plan;
+    if (!P) return fail(DGT_EINVAL, "null plan");
+    if (W < 0) return fail(DGT_EINVAL, "W < 0");
+    if (W == 0) return DGT_OK;
+    if (!f || !c) return fail(DGT_EINVAL, "null pointer");
+    const char* fb = (const char*)f;
+    const char* cb = (const char*)c;
+    const size_t fbytes = (size_t)W * P->info.L * P->esz, cbytes = (size_t)W * P->info.M * P->info.N * P->esz;
+    if (fb < cb + cbytes && cb < fb + fbytes) return fail(DGT_EINVAL, "f and c alias");
+    return execute_inverse(P, c, f, W, (cudaStream_t)cuda_stream);
 }
 
 int dgt_execute_host(dgt_plan_t plan, const void* f_host, void* c_host, int64_t W, void* cuda_stream) {

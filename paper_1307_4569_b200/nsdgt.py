@@ -43,7 +43,8 @@ class KernelStat(ctypes.Structure):
                 ("bytes", ctypes.c_double), ("flops", ctypes.c_double)]
 
 
-EXPORTS = ["dgt_lattice_plan", "dgt_plan", "dgt_execute", "dgt_execute_host", "dgt_destroy", "dgt_plan_query",
+EXPORTS = ["dgt_lattice_plan", "dgt_plan", "dgt_execute", "dgt_execute_inverse", "dgt_execute_host", "dgt_destroy",
+           "dgt_plan_query",
            "dgt_launches_per_execute", "dgt_profile_begin", "dgt_profile_end", "dgt_strerror", "dgt_last_error",
            "dgt_last_lmin", "dgt_version"]
 
@@ -54,6 +55,8 @@ _lib.dgt_plan.argtypes = [ctypes.POINTER(_P)] + [_I64] * 5 + [_P, _INT, _INT, _I
 _lib.dgt_plan.restype = _INT
 _lib.dgt_execute.argtypes = [_P, _P, _P, _I64, _P]
 _lib.dgt_execute.restype = _INT
+_lib.dgt_execute_inverse.argtypes = [_P, _P, _P, _I64, _P]
+_lib.dgt_execute_inverse.restype = _INT
 _lib.dgt_execute_host.argtypes = [_P, _P, _P, _I64, _P]
 _lib.dgt_execute_host.restype = _INT
 _lib.dgt_destroy.argtypes = [_P]
@@ -206,6 +209,26 @@ class Plan:
             raise TypeError("bad output tensor")
         _check(_lib.dgt_execute(self._h, ctypes.c_void_p(f2.data_ptr()), ctypes.c_void_p(out.data_ptr()), W,
                                 _stream_ptr(stream)), "dgt_execute")
+        return out[0] if squeeze else out
+
+    def inverse(self, c, out=None, stream=None):
+        """f[W, L] (CUDA tensor, complex) = synthesis of c[W, M, N] (CUDA tensor) with the plan's
+        window as the synthesis window (dgt_execute_inverse); 2-D c gives f[L].  A plan built
+        with the canonical dual window inverts the DGT of a plan built with the window."""
+        import torch
+        if not (isinstance(c, torch.Tensor) and c.is_cuda):
+            raise TypeError("inverse() takes a CUDA tensor")
+        squeeze = c.dim() == 2
+        c2 = c.reshape(1, self.M, self.N) if squeeze else c
+        if c2.dtype != self._cdt or not c2.is_contiguous() or tuple(c2.shape[1:]) != (self.M, self.N):
+            raise TypeError(f"c must be a contiguous {self._cdt} tensor of shape (W, M, N)")
+        W = c2.shape[0]
+        if out is None:
+            out = torch.empty((W, self.L), dtype=self._cdt, device=c.device)
+        elif out.dtype != self._cdt or not out.is_contiguous() or out.numel() != W * self.L:
+            raise TypeError("bad output tensor")
+        _check(_lib.dgt_execute_inverse(self._h, ctypes.c_void_p(c2.data_ptr()), ctypes.c_void_p(out.data_ptr()), W,
+                                        _stream_ptr(stream)), "dgt_execute_inverse")
         return out[0] if squeeze else out
 
     def execute_host(self, f, out=None, stream=None):
