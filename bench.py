@@ -26,6 +26,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 METRIC = "DGT coefficients/sec (W*M*N per s)"
+METRIC_INV = "DGT synthesis (inverse) coefficients/sec (W*M*N per s)"
 UNIT = "coefficients/s"
 
 
@@ -165,6 +166,26 @@ def oracle_sample(wl, budget_s, max_signals=None):
     return coefs / dt, cores, desc, dt
 
 
+def oracle_sample_inverse(wl, budget_s):
+    """Time the CPU oracle's synthesis (S2 regrouped, as it stands) on whole signals of the
+    workload until ~budget_s (at least one signal).  Returns (coefs/s, cores, description, s)."""
+    import numpy as np
+
+    import oracle
+    from synthetic import window
+    g = window(wl)
+    cores = oracle.threads()
+    rng = np.random.default_rng(0)
+    c = rng.standard_normal((1, wl.M, wl.N)) + 1j * rng.standard_normal((1, wl.M, wl.N))
+    n, t0 = 0, time.perf_counter()
+    while n == 0 or (time.perf_counter() - t0 < budget_s and n < wl.W):
+        oracle.idgt(c, g, wl.a, wl.M, wl.lam1, wl.lam2, variant="regrouped")
+        n += 1
+    dt = time.perf_counter() - t0
+    desc = f"oracle S2 regrouped synthesis (fp64, OpenMP), {n} whole signal(s) of {wl.name}"
+    return n * wl.M * wl.N / dt, cores, desc, dt
+
+
 def run_reference(args, wl, ws, rank):
     """--impl reference: the oracle on the host cores (rank 0 only)."""
     if rank != 0:
@@ -207,6 +228,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--force-generic", action="store_true")
     ap.add_argument("--max-chunk", type=int, default=0)
+    ap.add_argument("--inverse", action="store_true",
+                    help="time the synthesis (dgt_execute_inverse, c -> f) instead of the forward DGT")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -241,9 +264,20 @@ def main():
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
 
+    if args.inverse:
+        # synthesis: the step maps the coefficients of this rank's shard back to signals
+        plan.execute(f_dev, out=c_dev)
+        fo_dev = torch.empty((Wr, wl.L), dtype=cdt, device=dev)
+
+        def step():
+            plan.inverse(c_dev, out=fo_dev)
+    else:
+        def step():
+            plan.execute(f_dev, out=c_dev)
+
     # warm-up
     for _ in range(args.warmup):
-        plan.execute(f_dev, out=c_dev)
+        step()
     torch.cuda.synchronize()
 
     # timed region: K steps bracketed by barrier + synchronize, CUDA events on the launch stream;
@@ -257,7 +291,7 @@ def main():
     with sampler:
         e0.record(stream)
         for _ in range(args.steps):
-            plan.execute(f_dev, out=c_dev)
+            step()
         e1.record(stream)
         torch.cuda.synchronize()
     barrier(ws)
@@ -287,7 +321,7 @@ def main():
 
     # end to end through the C ABI with HOST buffers (pinned), copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.inverse:
         c_host = torch.empty((Wr, wl.M, wl.N), dtype=cdt, pin_memory=True)
         plan.execute_host(f_host, out=c_host)  # allocate staging outside the timed region
         ee0 = torch.cuda.Event(enable_timing=True)
@@ -309,19 +343,21 @@ def main():
                "path": "dgt_execute_host: pinned host f -> H2D (stream 1) -> kernels -> D2H (stream 2), chunked"}
         del c_host
 
-    launches = args.steps * plan.launches(Wr)
+    # our kernels only (the frequency-shear cuFFT calls are library launches)
+    launches = (sum(k["launches"] for k in stats if k["name"] != "front_fft_cufft") if args.inverse
+                else args.steps * plan.launches(Wr))
     launches_total = int(allreduce_sum(launches, ws))
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        v, cores, desc, dt = oracle_sample(wl, args.cpu_budget)
+        v, cores, desc, dt = (oracle_sample_inverse if args.inverse else oracle_sample)(wl, args.cpu_budget)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc, "seconds": dt}
 
     clocks = sampler.summary()
     if rank == 0:
         info = plan.info
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": METRIC_INV if args.inverse else METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded, synthetic/workloads.py)",
             "config": {"workload": wl.name, "L": wl.L, "a": wl.a, "M": wl.M, "N": wl.N,

@@ -896,9 +896,10 @@ struct Plan {
 };
 
 enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_ZAKADJ = 6,
-                PK_OUTADJ = 7, PK_COUNT = 8 };
+                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_COUNT = 9 };
 static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
-                                           "zak_ct_d180", "out_f4096", "zak_adjoint", "out_adjoint"};
+                                           "zak_ct_d180", "out_f4096", "zak_adjoint", "out_adjoint",
+                                           "fused7a_t_p1"};
 
 static cudaEvent_t prof_event(Plan* P) {
     if (P->pool_used == P->pool.size()) {
@@ -1278,6 +1279,18 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
 
 static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
+    if (P->fast && !std::getenv("NSDGT_INV_GENERIC")) {
+        // fused synthesis (fused7_adj.cuh) on the forward ring
+        const int ph = prof_open(P, st);
+        int rc = launch_fast_adj(&P->fp, c, P->Cws, f, W, st);
+        if (rc) return rc;
+        const double L = (double)I.L, MN = (double)I.M * (double)I.N;
+        prof_close(P, ph, PK_FASTADJ, W * (L + MN) * 8.0 + L * 8.0,
+                   W * (8.0 * L * I.q + 4.0 * L * std::log2((double)I.d) + 4.0 * MN * std::log2((double)I.d) +
+                        4.0 * MN * std::log2((double)I.iM) + 6.0 * MN), st);
+        CUDA_TRY(cudaGetLastError());
+        return DGT_OK;
+    }
     if (!P->Cinv) {
         CUDA_TRY(cudaMalloc(&P->Cinv, (size_t)P->inv_chunk * I.iM * I.iN * P->esz));
         if (I.branch == DGT_BRANCH_FREQ) CUDA_TRY(cudaMalloc(&P->finv, (size_t)P->inv_chunk * I.L * P->esz));

@@ -17,6 +17,7 @@
 #include "../../include/nsdgt.h"
 #include "cplx.cuh"
 #include "fused7.cuh"
+#include "fused7_adj.cuh"
 
 namespace nsdgt {
 
@@ -37,12 +38,18 @@ struct FastPlan {
     int minb = 3;                // CTAs per SM the kernel is compiled for
     const void* E = nullptr;     // Alg. 1 column phases (plan-owned)
     void* Gp = nullptr;          // G' (owned)
+    void* Gpa = nullptr;         // G' in the adjoint kernel's order (owned)
+    size_t smem_adj = 0;
     int* counters = nullptr;     // job queue + per-slot completion counters (owned)
 };
 
 template <int D, int MINB>
 static void launch7(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
     v7::fused7_kernel<D, MINB><<<grid, v7::Cfg<D>::NT, smem, st>>>(a);
+}
+template <int D, int MINB>
+static void launch7a(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
+    v7::fused7a_kernel<D, MINB><<<grid, v7::Cfg<D>::NT, smem, st>>>(a);
 }
 
 // Decide and build.  Returns DGT_OK with fp->kind == 0 when the lattice does not qualify.
@@ -83,6 +90,12 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     // registers).  NSDGT_CTAS overrides (experiments).
     int minb = D == 512 ? 3 : 5;
     if (const char* e = std::getenv("NSDGT_CTAS")) minb = std::max(3, std::min(D == 512 ? 4 : 5, std::atoi(e)));
+    {
+        const void* ka = D == 512 ? (const void*)v7::fused7a_kernel<512, 3> : (const void*)v7::fused7a_kernel<256, 5>;
+        const size_t sm = D == 512 ? v7::Cfg<512>::SMEM : v7::Cfg<256>::SMEM;
+        if (cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return DGT_ECUDA;
+        fp->smem_adj = sm;
+    }
     const void* kfn = D == 512 ? (minb == 4 ? (const void*)v7::fused7_kernel<512, 4> : (const void*)v7::fused7_kernel<512, 3>)
                                : (minb == 5   ? (const void*)v7::fused7_kernel<256, 5>
                                   : minb == 4 ? (const void*)v7::fused7_kernel<256, 4>
@@ -103,6 +116,12 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     if (cudaMalloc(&fp->Gp, sizeof(float2) * (size_t)M * Q * D) != cudaSuccess) { cudaFree(G64); return DGT_ENOMEM; }
     ga.Gp = (float4*)fp->Gp; ga.G64 = G64; ga.L = L; ga.K = K;
     ga.M = (int)M; ga.D = (int)D; ga.Q = (int)Q; ga.c = (int)I.c; ga.beta = (int)beta; ga.R1 = (int)(D / 16);
+    ga.layout = 0;
+    v7::k_gprime<<<(unsigned)std::min<int64_t>((M * Q * D + 255) / 256, 148 * 64), 256, 0, st>>>(ga);
+    // the same table in the synthesis kernel's order
+    if (cudaMalloc(&fp->Gpa, sizeof(float2) * (size_t)M * Q * D) != cudaSuccess) { cudaFree(G64); return DGT_ENOMEM; }
+    ga.Gp = (float4*)fp->Gpa;
+    ga.layout = 1;
     v7::k_gprime<<<(unsigned)std::min<int64_t>((M * Q * D + 255) / 256, 148 * 64), 256, 0, st>>>(ga);
     const cudaError_t err = cudaStreamSynchronize(st);
     cudaFree(G64);
@@ -140,6 +159,8 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
 
 inline void free_fast(FastPlan* fp) {
     if (fp->Gp) cudaFree(fp->Gp);
+    if (fp->Gpa) cudaFree(fp->Gpa);
+    fp->Gpa = nullptr;
     if (fp->counters) cudaFree(fp->counters);
     fp->Gp = nullptr;
     fp->counters = nullptr;
@@ -177,6 +198,38 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
     }
     if (fp->D == 512) (fp->minb == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st);
     else (fp->minb == 5 ? launch7<256, 5> : fp->minb == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st);
+    return DGT_OK;
+}
+
+// synthesis (fused7_adj.cuh): c (device, W x M x N) -> f (device, W x L), the ring as workspace.
+// The grid is the forward kernel's: 3 CTAs/SM for D = 512, 5 for D = 256 (both kernels use the
+// same shared memory and fewer registers for the adjoint; the occupancy query checks it).
+inline int launch_fast_adj(FastPlan* fp, const void* c, void* ws, void* f, int64_t W, cudaStream_t st) {
+    if (fp->kind != 2) return DGT_EUNSUPPORTED;
+    if (W * (int64_t)(fp->nA + fp->nB) >= (int64_t)1 << 31) return DGT_EUNSUPPORTED;
+    const int nctr = 1 + 2 * fp->S;
+    if (!fp->counters) {
+        if (cudaMalloc(&fp->counters, sizeof(int) * nctr) != cudaSuccess) return DGT_ENOMEM;
+    }
+    if (cudaMemsetAsync(fp->counters, 0, sizeof(int) * nctr, st) != cudaSuccess) return DGT_ECUDA;
+    v7::Args a{};
+    a.f = (const float2*)c; a.out = (float2*)f; a.ws = (float2*)ws; a.Gp = (const float4*)fp->Gpa;
+    a.E = (const float2*)fp->E; a.ctr = fp->counters; a.W = (int)W; a.N = fp->N; a.c = fp->c; a.Kmod = fp->Kmod;
+    a.beta = fp->beta; a.S = fp->S; a.lag = fp->lag; a.nA = fp->nA; a.nB = fp->nB;
+    a.dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;
+    int grid = fp->grid;
+    {
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const void* ka = fp->D == 512 ? (const void*)v7::fused7a_kernel<512, 3> : (const void*)v7::fused7a_kernel<256, 5>;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ka, v7::Cfg<512>::NT, fp->smem_adj) != cudaSuccess ||
+            per_sm < 1)
+            return DGT_ECUDA;
+        grid = std::min(grid, per_sm * sms);   // every CTA of the persistent grid resident
+    }
+    if (fp->D == 512) launch7a<512, 3>(a, grid, fp->smem_adj, st);
+    else launch7a<256, 5>(a, grid, fp->smem_adj, st);
     return DGT_OK;
 }
 

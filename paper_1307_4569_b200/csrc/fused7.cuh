@@ -582,6 +582,7 @@ struct GpArgs {
     const double2* G64;    // [(r*Q + u)*D + nu] = conj(Gamma_r(u; nu))/d
     int64_t L, K;          // chirp exponent K = sigma (L+1) mod 2L
     int M, D, Q, c, beta, R1;
+    int layout;            // 0: fused7 stage-1 order; 1: fused7a stage-2 order [j/8][h][r][m2][col][oi][u]
     int alpha[16];         // alpha_{l,u}, l,u < Q
 };
 
@@ -608,10 +609,18 @@ __global__ void k_gprime(GpArgs a) {
         const double vr = g.x * pr - g.y * pi, vi = g.x * pi + g.y * pr;
         // layout [j / 8][h][kp][t][slot][2]: j = 8 jb + 2 h + col, slot = 4 col + u, mu = t + 16 k,
         // k = 2 kp + hh (the order one product tile of fused7_kernel reads it)
-        const int t = mu & 15, k = mu >> 4;
         const int jb = j / 8, hq = (j % 8) / 2, col = j % 2, sl = 4 * col + u;
-        float2* dst = reinterpret_cast<float2*>(a.Gp) +
-                      (((((int64_t)jb * 4 + hq) * (a.R1 / 2) + (k >> 1)) * 16 + t) * 8 + sl) * 2 + (k & 1);
+        float2* dst;
+        if (a.layout == 0) {
+            const int t = mu & 15, k = mu >> 4;
+            dst = reinterpret_cast<float2*>(a.Gp) +
+                  (((((int64_t)jb * 4 + hq) * (a.R1 / 2) + (k >> 1)) * 16 + t) * 8 + sl) * 2 + (k & 1);
+        } else {
+            // mu = 16 r + oi + R1 m2 (the stage-2 output index of lane oi, round r)
+            const int r = (mu % a.R1) >> 4, oi = (mu % a.R1) & 15, m2 = mu / a.R1;
+            dst = reinterpret_cast<float2*>(a.Gp) +
+                  ((((((int64_t)jb * 4 + hq) * (a.R1 / 16) + r) * 16 + m2) * 2 + col) * 64 + oi * 4 + u);
+        }
         *dst = make_float2((float)vr, (float)vi);
     }
 }

@@ -1,0 +1,170 @@
+// fused7_adj.cuh -- synthesis (the adjoint of fused7) for the same lattices: time shear /
+// separable, p = 1, q = 4, d = M in {256, 512}, complex64 (BASELINE configs 3 and 5).
+// DESIGN.md §4.5.  The plan's window is the synthesis window gamma (pass the canonical dual
+// to invert); f = sum c(m,n) M_{b(m+w(n))} T_{an} gamma, the inversion formula of
+// PAPER.md:171-175.
+//
+// fused7 computes, per signal (fused7.cuh header):
+//   pass A, column j:  F_j(mu) = sum_s f(j + sM) W^{s mu};  x_{j,u}(mu) = F_j((sigma_j - mu) mod D) G'_{j,u}(mu);
+//                      ws[j][n] = DFT_D[x_{j,u}](n'),  n = kappa + q n', kappa = (l - u) mod q
+//   pass B, column n:  c[m][n] = E(n) sum_j ws[j][n] W^{j m}
+// Its adjoint runs the passes in the opposite order, every map replaced by its adjoint and
+// every inverse DFT computed as conj(DFT(conj(.))) on the same tile machinery:
+//   pass B', column n: ws'[j][n] = conj(E(n) Y_n(j)),  Y_n = DFT_M[conj(c[.][n])]
+//   pass A', column j: X_{j,u} = DFT_D[conj(ws'[j][kappa + q .])],
+//                      Fc_j(nu) = sum_u G'_{j,u}(mu) X_{j,u}(mu) at nu = (sigma_j - mu) mod D
+//                      (= conj of the adjoint's F'_j; the sum over u is a shuffle reduction:
+//                      the four u of a column sit in lanes L, L^8, L^16, L^24 of one warp),
+//                      f(j + sM) = conj(DFT_D[Fc_j](s)).
+// The ring ws (same slots and line layout as fused7: row j holds the N columns n in natural
+// order) now carries pass B' -> pass A'; each A' job is the only reader of its eight rows and
+// discards them from L2 afterwards.  Jobs: B'(w) (16 columns n) are queued lag signals ahead
+// of A'(w) (8 columns j); B'(w) waits until slot w mod S is free (all A'(w - S) done), A'(w)
+// waits for all B'(w).  The window table is G' of fused7 stored in the stage-2 (output)
+// order of a product tile (k_gprime layout 1).
+#pragma once
+#include "fused7.cuh"
+
+namespace nsdgt {
+namespace v7 {
+
+__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+
+// A (the fused7 Args): f = coefficients c [W][M][N] (input), out = signal [W][L] (output),
+// Gp = G' in layout 1 (float2 view).
+template <int D, int MINB>
+__global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
+    using K = Cfg<D>;
+    constexpr int R1 = K::R1, NR = K::NR, Q = K::Q, M = D, AC = K::ACOL;
+    constexpr int N = Q * D;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* X2 = reinterpret_cast<float2*>(smem_raw);
+    float2* F = X2 + K::XE;        // Fc[col * FS + nu], col < ACOL
+    float2* twt = F + K::FE;
+    __shared__ int jobsm;
+    const int tid = threadIdx.x;
+    const int s8 = tid & 7, h8 = tid >> 3;                  // roles S1 / M1
+    const int wq = tid >> 5, ln = tid & 31;                 // role M3 (product tiles, stage 2)
+    const int colM = wq >> 1, uM = ln >> 3, iM = (ln & 7) + 8 * (wq & 1);
+    for (int e = tid; e < 16 * R1; e += K::NT) {
+        const int tt = e / R1, m = e % R1;
+        double sn, cs;
+        sincospi(-2.0 * (double)((tt * m) % D) / (double)D, &sn, &cs);
+        twt[tt * K::TWS + m] = make_float2((float)cs, (float)sn);
+    }
+    const float2* tw = twt + h8 * K::TWS;
+    auto mark = [](int) {};
+    auto none = [] {};
+    int* queue = A.ctr;
+    int* doneB = A.ctr + 1;
+    int* doneA = A.ctr + 1 + A.S;
+    const int64_t MN = (int64_t)M * N;
+    const int64_t L = (int64_t)M * D;
+    const float2* Gq = reinterpret_cast<const float2*>(A.Gp);
+    float2 pre[R1];
+    int* pend = nullptr;
+    for (;;) {
+        // the previous job's shared-memory readers are done and its stores (and L2 discards)
+        // are ordered before thread 0's completion signal
+        __syncthreads();
+        if (tid == 0) {
+            if (pend) {
+                __threadfence();
+                atomicAdd(pend, 1);
+                pend = nullptr;
+            }
+            jobsm = atomicAdd(queue, 1);
+        }
+        __syncthreads();
+        int isB, w, idx;
+        if (!decode(jobsm, A.W, A.lag, A.nB, A.nA, &isB, &w, &idx)) break;
+        const int gen = w / A.S, slot = w - gen * A.S;
+        float2* wsl = A.ws + (int64_t)slot * MN;
+        if (tid == 0 && !(A.dbg & 1)) {
+            // B': slot free (all A'(w - S) done); A': all B'(w) done
+            if (isB) spin_until(doneA + slot, gen * A.nA);
+            else spin_until(doneB + slot, (gen + 1) * A.nB);
+        }
+        __syncthreads();   // every thread's ring accesses follow thread 0's acquire
+        if (isB) {
+            // ---------------- pass B': columns n = 16 idx .. 16 idx + 15 ----------------
+#pragma unroll 1
+            for (int bt = 0; bt < 2; ++bt) {
+                const int n = idx * 16 + 8 * bt + s8;
+                const float2 e = ldg_na2(A.E + n);
+                const float2* src = A.f + (int64_t)w * MN + n;
+#pragma unroll
+                for (int k = 0; k < R1; ++k) pre[k] = conjf2(ldg_na2(src + (int64_t)(h8 + 16 * k) * N));
+                if (bt) __syncthreads();   // previous tile's readers are done with X2
+                dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, none, none,
+                            [&](int r, const float2* y) {
+#pragma unroll
+                                for (int m2 = 0; m2 < 16; ++m2) {
+                                    const int j = 16 * r + h8 + R1 * m2;
+                                    wsl[(int64_t)j * N + n] = conjf2(cmw(y[m2], e));
+                                }
+                            }, A.dbg, mark);
+            }
+            if (tid == 0) pend = doneB + slot;
+        } else {
+            // ---------------- pass A': columns j0 .. j0 + 7 ----------------
+            const int j0 = idx * AC;
+#pragma unroll 1
+            for (int h = 0; h < 4; ++h) {
+                // stage-1 slot s8 = (column j0 + 2h + (s8 >> 2), u = s8 & 3), lane t = h8:
+                // conj(ws'[j][kappa + q (t + 16 k)])
+                const int jS = j0 + 2 * h + (s8 >> 2);
+                const int kapS = ((jS / A.c - (s8 & 3)) % Q + Q) % Q;
+                const float2* src = wsl + (int64_t)jS * N + kapS + 4 * h8;
+#pragma unroll
+                for (int k = 0; k < R1; ++k) pre[k] = conjf2(ld_cg(src + 64 * k));
+                __syncthreads();   // previous tile's readers are done with X2
+                const int jM = j0 + 2 * h + colM;
+                const int sig = (int)((((int64_t)jM * A.beta - ((int64_t)A.Kmod * jM) % D) % D + D) % D);
+                float2* Fc = F + (2 * h + colM) * K::FS;
+                // G' in stage-2 order: [j0/8][h][r][m2][col][oi][u]
+                const float2* g = Gq + ((((int64_t)idx * 4 + h) * NR * 16) * 2 + colM) * 64 + iM * 4 + uM;
+                dft_tile<D>(pre, tw, X2, s8, h8, 4 * colM + uM, iM, none, none,
+                            [&](int r, const float2* y) {
+#pragma unroll
+                                for (int m2 = 0; m2 < 16; ++m2) {
+                                    float2 p = cmw(y[m2], ldg_na2(g + ((int64_t)(r * 16 + m2) * 2) * 64));
+                                    p.x += __shfl_xor_sync(0xffffffffu, p.x, 8);
+                                    p.y += __shfl_xor_sync(0xffffffffu, p.y, 8);
+                                    p.x += __shfl_xor_sync(0xffffffffu, p.x, 16);
+                                    p.y += __shfl_xor_sync(0xffffffffu, p.y, 16);
+                                    const int mu = 16 * r + iM + R1 * m2;
+                                    if (uM == (m2 & 3)) Fc[(sig - mu) & (D - 1)] = p;
+                                }
+                            }, A.dbg, mark);
+            }
+            __syncthreads();   // Fc complete; X2 free
+            // Zak' tile: slot s8 = column j0 + s8, lane t = h8: Fc(t + 16 k)
+#pragma unroll
+            for (int k = 0; k < R1; ++k) pre[k] = F[s8 * K::FS + h8 + 16 * k];
+            float2* dst = A.out + (int64_t)w * L + j0 + s8;
+            dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, none, none,
+                        [&](int r, const float2* y) {
+#pragma unroll
+                            for (int m2 = 0; m2 < 16; ++m2) {
+                                const int s = 16 * r + h8 + R1 * m2;
+                                __stcs(dst + (int64_t)s * M, conjf2(y[m2]));
+                            }
+                        }, A.dbg, mark);
+            // the eight ring rows this job read are dead: drop them from L2
+            constexpr int LPR = N / 16;   // 128-byte lines per row
+            for (int e = tid; e < AC * LPR; e += K::NT)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(wsl + (int64_t)(j0 + e / LPR) * N + (e % LPR) * 16)
+                             : "memory");
+            if (tid == 0) pend = doneA + slot;
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && pend) {
+        __threadfence();
+        atomicAdd(pend, 1);
+    }
+}
+
+}  // namespace v7
+}  // namespace nsdgt

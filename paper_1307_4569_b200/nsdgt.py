@@ -184,11 +184,11 @@ class Plan:
 
     def profile_end(self) -> list:
         """Synchronise the recorded events; per kernel kind: launches, ms, algorithmic bytes, flops."""
-        stats = (KernelStat * 8)()
+        stats = (KernelStat * 16)()
         n = ctypes.c_int(0)
-        _check(_lib.dgt_profile_end(self._h, stats, 8, ctypes.byref(n)), "dgt_profile_end")
+        _check(_lib.dgt_profile_end(self._h, stats, 16, ctypes.byref(n)), "dgt_profile_end")
         return [{"name": stats[i].name.decode(), "launches": int(stats[i].launches), "ms": float(stats[i].ms),
-                 "bytes": float(stats[i].bytes), "flops": float(stats[i].flops)} for i in range(min(n.value, 8))]
+                 "bytes": float(stats[i].bytes), "flops": float(stats[i].flops)} for i in range(min(n.value, 16))]
 
     def execute(self, f, out=None, stream=None):
         """c[W, M, N] (CUDA tensor) = DGT of f[W, L] (CUDA tensor); 1-D f gives c[M, N]."""

@@ -137,3 +137,23 @@ def test_inverse_errors_and_empty(torch_cuda, nsdgt):
     assert e.shape == (0, L)
     with pytest.raises(TypeError):
         plan.inverse(torch.zeros((1, M, L // a), dtype=torch.complex128, device="cuda"))
+
+
+@pytest.mark.parametrize("k,W", [(3, 1), (3, 17), (3, 40), (5, 3), (5, 9)])
+def test_fused_synthesis_matches_generic_and_oracle(torch_cuda, nsdgt, oracle_mod, k, W, monkeypatch):
+    """Configs 3 and 5 (fused7 lattices): the fused synthesis kernel (fused7_adj.cuh) against
+    the generic adjoint kernels on ragged batches, and one signal against the oracle."""
+    torch = torch_cuda
+    wl = CONFIGS[k - 1]
+    g = window(wl)
+    rng = np.random.default_rng(100 + W)
+    c = rand_c(rng, W, wl.M, wl.N, "c64")
+    ct = torch.from_numpy(c).cuda()
+    pf = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c64")
+    assert pf.info["kernel_path"] == 2
+    ff = pf.inverse(ct).cpu().numpy()
+    monkeypatch.setenv("NSDGT_INV_GENERIC", "1")
+    fg = pf.inverse(ct).cpu().numpy()
+    assert rel(ff, fg) <= TOL["c64"]
+    ref = oracle_mod.idgt(c[W - 1].astype(np.complex128), g, wl.a, wl.M, wl.lam1, wl.lam2)
+    assert rel(ff[W - 1], ref) <= TOL["c64"]
