@@ -88,15 +88,24 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
         __syncthreads();   // every thread's ring accesses follow thread 0's acquire
         if (isB) {
             // ---------------- pass B': columns n = 16 idx .. 16 idx + 15 ----------------
+            // tile bt's input: column n = 16 idx + 8 bt + s8, rows m = t + 16 k (conjugated when used)
+            auto load_c = [&](int bt) {
+                const float2* src = A.f + (int64_t)w * MN + idx * 16 + 8 * bt + s8;
+#pragma unroll
+                for (int k = 0; k < R1; ++k) pre[k] = ldg_na2(src + (int64_t)(h8 + 16 * k) * N);
+            };
 #pragma unroll 1
             for (int bt = 0; bt < 2; ++bt) {
                 const int n = idx * 16 + 8 * bt + s8;
                 const float2 e = ldg_na2(A.E + n);
-                const float2* src = A.f + (int64_t)w * MN + n;
+                if (bt == 0) load_c(0);
 #pragma unroll
-                for (int k = 0; k < R1; ++k) pre[k] = conjf2(ldg_na2(src + (int64_t)(h8 + 16 * k) * N));
+                for (int k = 0; k < R1; ++k) pre[k] = conjf2(pre[k]);
                 if (bt) __syncthreads();   // previous tile's readers are done with X2
-                dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, none, none,
+                dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, none,
+                            [&] {
+                                if (bt == 0) load_c(1);   // next tile's inputs behind this tile's stage 2
+                            },
                             [&](int r, const float2* y) {
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) {
@@ -109,22 +118,30 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
         } else {
             // ---------------- pass A': columns j0 .. j0 + 7 ----------------
             const int j0 = idx * AC;
-#pragma unroll 1
-            for (int h = 0; h < 4; ++h) {
-                // stage-1 slot s8 = (column j0 + 2h + (s8 >> 2), u = s8 & 3), lane t = h8:
-                // conj(ws'[j][kappa + q (t + 16 k)])
+            // product tile h's input: stage-1 slot s8 = (column j0 + 2h + (s8 >> 2), u = s8 & 3),
+            // lane t = h8: ws'[j][kappa + q (t + 16 k)] (conjugated when used)
+            auto load_r = [&](int h) {
                 const int jS = j0 + 2 * h + (s8 >> 2);
                 const int kapS = ((jS / A.c - (s8 & 3)) % Q + Q) % Q;
                 const float2* src = wsl + (int64_t)jS * N + kapS + 4 * h8;
 #pragma unroll
-                for (int k = 0; k < R1; ++k) pre[k] = conjf2(ld_cg(src + 64 * k));
+                for (int k = 0; k < R1; ++k) pre[k] = ld_cg(src + 64 * k);
+            };
+#pragma unroll 1
+            for (int h = 0; h < 4; ++h) {
+                if (h == 0) load_r(0);
+#pragma unroll
+                for (int k = 0; k < R1; ++k) pre[k] = conjf2(pre[k]);
                 __syncthreads();   // previous tile's readers are done with X2
                 const int jM = j0 + 2 * h + colM;
                 const int sig = (int)((((int64_t)jM * A.beta - ((int64_t)A.Kmod * jM) % D) % D + D) % D);
                 float2* Fc = F + (2 * h + colM) * K::FS;
                 // G' in stage-2 order: [j0/8][h][r][m2][col][oi][u]
                 const float2* g = Gq + ((((int64_t)idx * 4 + h) * NR * 16) * 2 + colM) * 64 + iM * 4 + uM;
-                dft_tile<D>(pre, tw, X2, s8, h8, 4 * colM + uM, iM, none, none,
+                dft_tile<D>(pre, tw, X2, s8, h8, 4 * colM + uM, iM, none,
+                            [&] {
+                                if (h < 3) load_r(h + 1);   // next tile's inputs behind this tile's stage 2
+                            },
                             [&](int r, const float2* y) {
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) {
