@@ -216,6 +216,13 @@ inline int launch_fast_adj(FastPlan* fp, const void* c, void* ws, void* f, int64
     a.f = (const float2*)c; a.out = (float2*)f; a.ws = (float2*)ws; a.Gp = (const float4*)fp->Gpa;
     a.E = (const float2*)fp->E; a.ctr = fp->counters; a.W = (int)W; a.N = fp->N; a.c = fp->c; a.Kmod = fp->Kmod;
     a.beta = fp->beta; a.S = fp->S; a.lag = fp->lag; a.nA = fp->nA; a.nB = fp->nB;
+    // Synthesis look-ahead: B' jobs are short (2 tiles) and the long A' jobs (5 tiles) free the
+    // ring slots, so A'(w) needs less lag behind B'(w) than fused7's B behind A, and a shorter
+    // lag leaves more slots between B'(w) and the A'(w - S) it waits for.  Measured: config 5
+    // lag 2 (S = 8) 6.24 ms against 8.07 ms at fused7's lag 5; config 3 lag 6 (S = 20) 0.39 ms
+    // against 0.48 ms at lag 14.
+    a.lag = std::max(1, std::min(fp->S - 1, (2 * fp->lag + 2) / 5));
+    if (const char* e = std::getenv("NSDGT_LAG_ADJ")) a.lag = std::max(0, std::min(fp->S - 1, std::atoi(e)));   // experiment
     a.dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;
     int grid = fp->grid;
     {
