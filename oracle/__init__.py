@@ -12,7 +12,11 @@ lowest non-negative frequency).  See ``dgt_oracle.c`` for the two evaluations
 ``idgt`` is the synthesis operator (the inverse DGT with a dual window, the inversion
 formula of PAPER.md:171-175), the adjoint of Eq. (DGT).
 
-Parity pinned for: ``dgt`` and ``idgt`` (both variants each).  Nothing here is "parity
+``windows.canonical_dual`` / ``windows.canonical_tight`` (numpy, dense frame operator of
+Eq. frameop) give the dual and tight windows for small L.
+
+Parity pinned for: ``dgt`` and ``idgt`` (both variants each), ``windows`` (S gamma = g through
+dgt/idgt, perfect reconstruction, tight energy identity; tests/test_oracle_pins.py).  Nothing here is "parity
 unpinned".
 """
 from __future__ import annotations
@@ -22,6 +26,8 @@ import os
 import subprocess
 
 import numpy as np
+
+from . import windows  # noqa: F401  (dense dual / tight windows)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dgt_oracle.c")

@@ -248,3 +248,33 @@ def test_idgt_literal_equals_regrouped_batch(oracle_mod, L, a, M, l1, l2):
     f2 = oracle_mod.idgt(c, gamma, a, M, l1, l2, variant="regrouped")
     assert f1.shape == (2, L) and rel(f1, f2) < 1e-13
     assert rel(oracle_mod.idgt(c[1], gamma, a, M, l1, l2), f2[1]) < 1e-13
+
+
+# ---- canonical dual / tight windows: oracle.windows ----
+
+# redundancy M/a > 1 (the Fig. 1 lattices are critically sampled; there the Gaussian system is
+# a near-singular frame and reconstruction is ill-conditioned)
+@pytest.mark.parametrize("L,a,M,l1,l2", [(36, 6, 12, 1, 3), (36, 4, 6, 1, 3), (36, 6, 12, 2, 3), (72, 8, 12, 1, 3),
+                                         (240, 8, 12, 1, 2), (120, 10, 12, 0, 1), (96, 8, 12, 1, 4)])
+def test_dual_window_defining_equation(oracle_mod, L, a, M, l1, l2):
+    """S gamma = g with S applied as idgt(dgt(., g), g) (the oracle's own, independently pinned
+    analysis and synthesis sums), and perfect reconstruction with gamma."""
+    g = pgauss(L, a * M / L)
+    gamma = oracle_mod.windows.canonical_dual(g, a, M, l1, l2)
+    Sg = oracle_mod.idgt(oracle_mod.dgt(gamma, g, a, M, l1, l2), g, a, M, l1, l2)
+    assert rel(Sg, g.astype(complex)) < 1e-11
+    f, _ = random_pair(L, 36)
+    fr = oracle_mod.idgt(oracle_mod.dgt(f, g, a, M, l1, l2), gamma, a, M, l1, l2)
+    assert rel(fr, f.astype(complex)) < 1e-11
+
+
+@pytest.mark.parametrize("L,a,M,l1,l2", [(36, 6, 6, 1, 2), (72, 8, 12, 1, 3), (240, 8, 12, 1, 2)])
+def test_tight_window_properties(oracle_mod, L, a, M, l1, l2):
+    """g_t = S^{-1/2} g: the system of g_t is a Parseval frame -- perfect reconstruction with
+    itself and ||c||^2 = ||f||^2 (S_{g_t} = I)."""
+    g = pgauss(L, a * M / L)
+    gt = oracle_mod.windows.canonical_tight(g, a, M, l1, l2)
+    f, _ = random_pair(L, 37)
+    c = oracle_mod.dgt(f, gt, a, M, l1, l2)
+    assert abs(np.linalg.norm(c) ** 2 / np.linalg.norm(f) ** 2 - 1.0) < 1e-11
+    assert rel(oracle_mod.idgt(c, gt, a, M, l1, l2), f.astype(complex)) < 1e-11
