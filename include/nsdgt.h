@@ -40,6 +40,8 @@ typedef enum dgt_status {
                                 lambda1 not in [0, lambda2), gcd(lambda1,lambda2) != 1 (unless
                                 lambda = 0/1), W < 0, bad dtype/flags, f and c alias, or an
                                 explicit shear that violates Eq. (modcond) */
+    DGT_ENUMERIC = 3,        /* dgt_window_dual only: the window does not generate a frame on the
+                                lattice (a factor of the frame operator is singular) */
     DGT_EILLEGAL_LENGTH = 4, /* L is not a multiple of L_min = lambda2*lcm(a,M) (Prop. minsig,
                                 PAPER.md:580-615); dgt_last_lmin() reports L_min */
     DGT_ECUDA = 5,           /* a CUDA runtime call failed (dgt_last_error() has the text) */
@@ -121,6 +123,20 @@ int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_s
  * (adjoint) kernels for every lattice.  W = 0 is a no-op.
  * Errors: DGT_EINVAL (null/aliasing, W < 0), DGT_ECUDA, DGT_ECUFFT, DGT_ENOMEM. */
 int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void* cuda_stream);
+
+/* Canonical dual (kind 0, S^{-1} g) or canonical tight (kind 1, S^{-1/2} g) window of the plan's
+ * window on the plan's lattice: Alg. 2 of PAPER.md:951-994 -- the plan's shear
+ * (chirp, and for the frequency shear the length-L FFT), the separable dual/tight window by the
+ * factorisation of the frame operator (per (r, nu) the p x p matrix
+ * H = Gamma Gamma^H, dual factor H^{-1} Gamma / M', tight factor H^{-1/2} Gamma / sqrt(M')),
+ * then the shear undone.  fp64 throughout, rounded once to the plan's dtype.
+ * out: L complex of the plan's dtype, host memory when flags has DGT_G_ON_HOST, else device.
+ * Synchronous on cuda_stream; allocates and frees its fp64 workspace.  S is the frame operator
+ * of Eq. (frameop); a plan built with the dual window inverts the DGT
+ * through dgt_execute_inverse.
+ * Errors: DGT_EINVAL, DGT_EUNSUPPORTED (p > 8 or q > 64; tight with p > 2), DGT_ENUMERIC,
+ * DGT_ECUDA, DGT_ECUFFT, DGT_ENOMEM. */
+int dgt_window_dual(dgt_plan_t plan, int kind, void* out, int flags, void* cuda_stream);
 
 /* End-to-end variant with HOST buffers: copies f (host, W x L) to the device, runs the
  * transform and copies c (host, W x M x N) back, chunk by chunk with the copies overlapped

@@ -837,6 +837,140 @@ __global__ void k_conj_chirp(cx<T>* out, const cx<T>* in, const cx<T>* __restric
 }
 
 // ---------------------------------------------------------------------------------
+// canonical dual / tight window (Alg. 2 of PAPER.md:951-994 with the separable
+// dual by factorisation).  All in fp64, plan time.
+//
+// The plan's inner separable lattice transforms the window to g~ (T: P_{s1} g) or g^ (F:
+// P_{-s0} FFT(P_{s1} g) / L) with factorisation Gamma_r(k, u; nu) = sum_s g~(x(r,k,u,s))
+// W_d^{s nu} (p x q per (r, nu)).  With Z the factorisation map (Z* Z = d) the separable frame
+// operator is S = M' Z* (H (x) I) Z / d,  H = Gamma Gamma^H (p x p), so
+//   dual:  Z gamma~ = H^{-1} Gamma / M',      tight: Z g~_t = H^{-1/2} Gamma / sqrt(M')
+// (M' = iM, the inner channel count).  Then gamma~ = Z^{-1}(.) and the shear is undone:
+//   T: gamma = conj(P_{s1}) gamma~;   F: gamma = conj(P_{s1}) IFFT_unnorm(conj(P_{-s0}) gamma~) / L
+// (S_nonsep = V* S~ V with V = P_{-s0} F P_{s1}, V* V = L; the tight window takes 1/sqrt(L)
+// instead of 1/L).
+// ---------------------------------------------------------------------------------
+constexpr int kDualPMax = 8, kDualQMax = 64;
+
+// one thread per (r, nu); G64[((r q + u) p + k) d + nu] = conj(Gamma)/d  ->  Gd (same layout,
+// the factorisation Gamma^d of the result, NOT conjugated)
+__global__ void k_dual_factor(double2* Gd, const double2* G64, int64_t c, int64_t d, int p, int q, double scale,
+                              int tight, int* status) {
+    for (int64_t rv = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; rv < c * d; rv += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = rv / d, nu = rv % d;
+        double2 Gm[kDualPMax][kDualQMax];
+        for (int k = 0; k < p; ++k)
+            for (int u = 0; u < q; ++u) {
+                const double2 v = G64[((r * q + u) * p + k) * d + nu];
+                Gm[k][u] = make_double2(v.x * (double)d, -v.y * (double)d);   // Gamma
+            }
+        double2 H[kDualPMax][kDualPMax];
+        for (int k = 0; k < p; ++k)
+            for (int k2 = 0; k2 < p; ++k2) {
+                double sr = 0.0, si = 0.0;
+                for (int u = 0; u < q; ++u) {   // Gamma[k][u] conj(Gamma[k2][u])
+                    sr += Gm[k][u].x * Gm[k2][u].x + Gm[k][u].y * Gm[k2][u].y;
+                    si += Gm[k][u].y * Gm[k2][u].x - Gm[k][u].x * Gm[k2][u].y;
+                }
+                H[k][k2] = make_double2(sr, si);
+            }
+        double2 X[kDualPMax][kDualPMax];   // the p x p left factor: H^{-1} or H^{-1/2}
+        if (!tight) {
+            // Gauss-Jordan on [H | I] with partial pivoting
+            for (int k = 0; k < p; ++k)
+                for (int k2 = 0; k2 < p; ++k2) X[k][k2] = make_double2(k == k2 ? 1.0 : 0.0, 0.0);
+            for (int col = 0; col < p; ++col) {
+                int piv = col;
+                double best = 0.0;
+                for (int k = col; k < p; ++k) {
+                    const double m2 = H[k][col].x * H[k][col].x + H[k][col].y * H[k][col].y;
+                    if (m2 > best) { best = m2; piv = k; }
+                }
+                if (best == 0.0) { atomicExch(status, 1); break; }
+                for (int k2 = 0; k2 < p; ++k2) {
+                    double2 t = H[col][k2]; H[col][k2] = H[piv][k2]; H[piv][k2] = t;
+                    t = X[col][k2]; X[col][k2] = X[piv][k2]; X[piv][k2] = t;
+                }
+                const double2 hv = H[col][col];
+                const double den = hv.x * hv.x + hv.y * hv.y;
+                const double2 inv = make_double2(hv.x / den, -hv.y / den);
+                for (int k2 = 0; k2 < p; ++k2) { H[col][k2] = cmul(H[col][k2], inv); X[col][k2] = cmul(X[col][k2], inv); }
+                for (int k = 0; k < p; ++k) {
+                    if (k == col) continue;
+                    const double2 fct = H[k][col];
+                    for (int k2 = 0; k2 < p; ++k2) {
+                        H[k][k2] = H[k][k2] - cmul(fct, H[col][k2]);
+                        X[k][k2] = X[k][k2] - cmul(fct, X[col][k2]);
+                    }
+                }
+            }
+        } else if (p == 1) {
+            X[0][0] = make_double2(1.0 / sqrt(H[0][0].x), 0.0);
+        } else {
+            // p = 2: sqrt(H) = (H + sqrt(det) I) / sqrt(tr + 2 sqrt(det)), then its inverse
+            const double det = H[0][0].x * H[1][1].x - (H[0][1].x * H[0][1].x + H[0][1].y * H[0][1].y);
+            const double sd = sqrt(det), tnorm = sqrt(H[0][0].x + H[1][1].x + 2.0 * sd);
+            const double a00 = (H[0][0].x + sd) / tnorm, a11 = (H[1][1].x + sd) / tnorm;
+            const double2 a01 = make_double2(H[0][1].x / tnorm, H[0][1].y / tnorm);
+            const double dr = a00 * a11 - (a01.x * a01.x + a01.y * a01.y);   // det(sqrt H) > 0
+            X[0][0] = make_double2(a11 / dr, 0.0);
+            X[1][1] = make_double2(a00 / dr, 0.0);
+            X[0][1] = make_double2(-a01.x / dr, -a01.y / dr);
+            X[1][0] = make_double2(-a01.x / dr, a01.y / dr);   // conj(a01)
+        }
+        for (int k = 0; k < p; ++k)
+            for (int u = 0; u < q; ++u) {
+                double sr = 0.0, si = 0.0;
+                for (int k2 = 0; k2 < p; ++k2) {
+                    const double2 t = cmul(X[k][k2], Gm[k2][u]);
+                    sr += t.x;
+                    si += t.y;
+                }
+                Gd[((r * q + u) * p + k) * d + nu] = make_double2(sr * scale, si * scale);
+            }
+    }
+}
+
+// gamma~(x(r,k,u,s)) = (1/d) sum_nu Gd_r(k,u;nu) W_d^{-s nu}, then the T-branch un-shear
+// conj(P_sigma(x)) (sigma = s1; 0 = none) or, F-branch, conj(P_{-s0}(x)) before the IFFT.
+__global__ void k_dual_unfactor(double2* out, const double2* Gd, int64_t L, int64_t c, int64_t d, int64_t p,
+                                int64_t q, int64_t sigma) {
+    const int64_t Lc = L / c;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i % d;
+        const int64_t k = (i / d) % p;
+        const int64_t u = (i / (d * p)) % q;
+        const int64_t r = i / (d * p * q);
+        const double2* src = Gd + ((r * q + u) * p + k) * d;
+        double sr = 0.0, si = 0.0;
+        int64_t e = 0;   // s nu mod d
+        for (int64_t nu = 0; nu < d; ++nu) {
+            double sn, cs;
+            sincospi(2.0 * (double)e / (double)d, &sn, &cs);
+            const double2 v = src[nu];
+            sr += v.x * cs - v.y * sn;
+            si += v.x * sn + v.y * cs;
+            e += s;
+            if (e >= d) e -= d;
+        }
+        const int64_t x = r + c * ((k * q + p * u + s * p * q) % Lc);
+        double2 v = make_double2(sr / (double)d, si / (double)d);
+        if (sigma) v = cmulc(v, chirp_val(sigma, x, L));
+        out[x] = v;
+    }
+}
+
+// F-branch tail: out = conj(P_{s1}(x)) in(x) / L (s1 = 0: the chirp is 1), cast to T
+template <typename T>
+__global__ void k_dual_finish(cx<T>* out, const double2* in, int64_t L, int64_t sigma, double scale) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < L; x += (int64_t)gridDim.x * blockDim.x) {
+        double2 v = in[x];
+        if (sigma) v = cmulc(v, chirp_val(sigma, x, L));
+        out[x] = mk<T>((T)(v.x * scale), (T)(v.y * scale));
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // the plan
 // ---------------------------------------------------------------------------------
 
@@ -848,6 +982,7 @@ struct Plan {
     size_t esz = 8;  // complex element size
     // device tables
     void* G = nullptr;       // window factors (L complex)
+    double2* gt64 = nullptr; // the Alg. 1 window transform g~ / g^ in fp64 (dual/tight windows)
     void* chirp = nullptr;   // kernel-A load multiplier (L complex) or null
     void* pre = nullptr;     // F-branch pre-FFT chirp (L complex) or null
     void* tw_d = nullptr;    // twiddles length d
@@ -931,7 +1066,7 @@ static void prof_close(Plan* P, int h, int kind, double bytes, double flops, cud
 static void free_plan(Plan* P) {
     if (!P) return;
     void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
-                    P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv};
+                    P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv, P->gt64};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     free_fast(&P->fp);
@@ -1023,7 +1158,7 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
     P->fast = P->fp.kind;
     CUDA_TRY(cudaStreamSynchronize(st));
     cudaFree(g_dev);
-    cudaFree(gt);
+    P->gt64 = gt;   // kept for dgt_window_dual
     return DGT_OK;
 }
 
@@ -1350,6 +1485,7 @@ const char* dgt_strerror(int status) {
     switch (status) {
         case DGT_OK: return "ok";
         case DGT_EINVAL: return "invalid argument";
+        case DGT_ENUMERIC: return "the window does not generate a frame on this lattice";
         case DGT_EILLEGAL_LENGTH: return "illegal transform length (L must be a multiple of L_min)";
         case DGT_ECUDA: return "CUDA runtime error";
         case DGT_ECUFFT: return "cuFFT error";
@@ -1436,6 +1572,68 @@ int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void
     const size_t fbytes = (size_t)W * P->info.L * P->esz, cbytes = (size_t)W * P->info.M * P->info.N * P->esz;
     if (fb < cb + cbytes && cb < fb + fbytes) return fail(DGT_EINVAL, "f and c alias");
     return execute_inverse(P, c, f, W, (cudaStream_t)cuda_stream);
+}
+
+int dgt_window_dual(dgt_plan_t plan, int kind, void* out, int flags, void* cuda_stream) {
+    Plan* P = (Plan*)plan;
+    if (!P || !out) return fail(DGT_EINVAL, "null pointer");
+    if (kind != 0 && kind != 1) return fail(DGT_EINVAL, "kind must be 0 (dual) or 1 (tight)");
+    if (flags & ~DGT_G_ON_HOST) return fail(DGT_EINVAL, "bad flags");
+    const dgt_lattice_info& I = P->info;
+    if (I.p > kDualPMax || I.q > kDualQMax) return fail(DGT_EUNSUPPORTED, "p or q too large for the dual kernel");
+    if (kind == 1 && I.p > 2) return fail(DGT_EUNSUPPORTED, "tight window implemented for p <= 2");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const int64_t L = I.L;
+    double2 *G64 = nullptr, *Gd = nullptr, *buf = nullptr;
+    int* status = nullptr;
+    int rc = DGT_OK;
+    auto cleanup = [&]() {
+        cudaFree(G64); cudaFree(Gd); cudaFree(buf); cudaFree(status);
+    };
+    if (cudaMalloc(&G64, sizeof(double2) * L) != cudaSuccess || cudaMalloc(&Gd, sizeof(double2) * L) != cudaSuccess ||
+        cudaMalloc(&buf, sizeof(double2) * L) != cudaSuccess || cudaMalloc(&status, sizeof(int)) != cudaSuccess) {
+        cleanup();
+        return fail(DGT_ENOMEM, "dual window workspace");
+    }
+    cudaMemsetAsync(status, 0, sizeof(int), st);
+    k_window_factor<double><<<grid_for(L), 256, 0, st>>>(G64, P->gt64, L, I.c, I.d, I.p, I.q);
+    const double scale = kind == 0 ? 1.0 / (double)I.iM : 1.0 / std::sqrt((double)I.iM);
+    k_dual_factor<<<grid_for(I.c * I.d, 64), 64, 0, st>>>(Gd, G64, I.c, I.d, (int)I.p, (int)I.q, scale, kind, status);
+    const bool freq = I.branch == DGT_BRANCH_FREQ;
+    // T: conj(P_{s1}) on the unfactored window; F: conj(P_{-s0}) before the inverse FFT
+    k_dual_unfactor<<<grid_for(L), 256, 0, st>>>(buf, Gd, L, I.c, I.d, I.p, I.q, freq ? -I.s0 : I.s1);
+    double2* res = buf;
+    if (freq) {
+        cufftHandle h;
+        if (cufftPlan1d(&h, (int)L, CUFFT_Z2Z, 1) != CUFFT_SUCCESS) { cleanup(); return fail(DGT_ECUFFT, "dual window FFT plan"); }
+        cufftSetStream(h, st);
+        const cufftResult fr = cufftExecZ2Z(h, (cufftDoubleComplex*)buf, (cufftDoubleComplex*)G64, CUFFT_INVERSE);
+        cudaStreamSynchronize(st);
+        cufftDestroy(h);
+        if (fr != CUFFT_SUCCESS) { cleanup(); return fail(DGT_ECUFFT, "dual window FFT"); }
+        res = G64;
+    }
+    // cast (and the F-branch conj(P_{s1}) / L) into a device buffer of the plan's dtype
+    void* dst = out;
+    void* tmp = nullptr;
+    if (flags & DGT_G_ON_HOST) {
+        if (cudaMalloc(&tmp, P->esz * L) != cudaSuccess) { cleanup(); return fail(DGT_ENOMEM, "dual window output"); }
+        dst = tmp;
+    }
+    const int64_t sig_fin = freq ? I.s1 : 0;
+    // V = P_{-s0} F P_{s1} has V* V = L: the dual carries 1/L, the tight window 1/sqrt(L)
+    const double sc_fin = freq ? (kind == 0 ? 1.0 / (double)L : 1.0 / std::sqrt((double)L)) : 1.0;
+    if (P->dtype == DGT_C64) k_dual_finish<float><<<grid_for(L), 256, 0, st>>>((float2*)dst, res, L, sig_fin, sc_fin);
+    else k_dual_finish<double><<<grid_for(L), 256, 0, st>>>((double2*)dst, res, L, sig_fin, sc_fin);
+    int hstatus = 0;
+    cudaError_t e = cudaMemcpyAsync(&hstatus, status, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && tmp) e = cudaMemcpyAsync(out, tmp, P->esz * L, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (tmp) cudaFree(tmp);
+    cleanup();
+    if (e != cudaSuccess) return fail(DGT_ECUDA, std::string("dual window: ") + cudaGetErrorString(e));
+    if (hstatus) return fail(DGT_ENUMERIC, "the window does not generate a frame on this lattice (singular factor)");
+    return rc;
 }
 
 int dgt_execute_host(dgt_plan_t plan, const void* f_host, void* c_host, int64_t W, void* cuda_stream) {

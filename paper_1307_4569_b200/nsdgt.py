@@ -43,7 +43,8 @@ class KernelStat(ctypes.Structure):
                 ("bytes", ctypes.c_double), ("flops", ctypes.c_double)]
 
 
-EXPORTS = ["dgt_lattice_plan", "dgt_plan", "dgt_execute", "dgt_execute_inverse", "dgt_execute_host", "dgt_destroy",
+EXPORTS = ["dgt_lattice_plan", "dgt_plan", "dgt_execute", "dgt_execute_inverse", "dgt_window_dual", "dgt_execute_host",
+           "dgt_destroy",
            "dgt_plan_query",
            "dgt_launches_per_execute", "dgt_profile_begin", "dgt_profile_end", "dgt_strerror", "dgt_last_error",
            "dgt_last_lmin", "dgt_version"]
@@ -57,6 +58,8 @@ _lib.dgt_execute.argtypes = [_P, _P, _P, _I64, _P]
 _lib.dgt_execute.restype = _INT
 _lib.dgt_execute_inverse.argtypes = [_P, _P, _P, _I64, _P]
 _lib.dgt_execute_inverse.restype = _INT
+_lib.dgt_window_dual.argtypes = [_P, _INT, _P, _INT, _P]
+_lib.dgt_window_dual.restype = _INT
 _lib.dgt_execute_host.argtypes = [_P, _P, _P, _I64, _P]
 _lib.dgt_execute_host.restype = _INT
 _lib.dgt_destroy.argtypes = [_P]
@@ -230,6 +233,14 @@ class Plan:
         _check(_lib.dgt_execute_inverse(self._h, ctypes.c_void_p(c2.data_ptr()), ctypes.c_void_p(out.data_ptr()), W,
                                         _stream_ptr(stream)), "dgt_execute_inverse")
         return out[0] if squeeze else out
+
+    def dual_window(self, tight: bool = False, stream=None) -> np.ndarray:
+        """Canonical dual (S^{-1} g) or tight (S^{-1/2} g) window of the plan's window on its
+        lattice, computed on the GPU (dgt_window_dual); returned as a host numpy array."""
+        out = np.empty(self.L, dtype=np.complex64 if self.dtype == "c64" else np.complex128)
+        _check(_lib.dgt_window_dual(self._h, 1 if tight else 0, ctypes.c_void_p(out.ctypes.data), DGT_G_ON_HOST,
+                                    _stream_ptr(stream)), "dgt_window_dual")
+        return out
 
     def execute_host(self, f, out=None, stream=None):
         """End-to-end call on HOST arrays (numpy or CPU tensors; pinned memory is faster)."""
