@@ -266,3 +266,27 @@ def test_errors_on_gpu(torch_cuda, nsdgt):
     plan = nsdgt.Plan(48, 4, 6, 1, 2, np.ones(48), dtype="c64")
     with pytest.raises(TypeError):
         plan.execute(torch.zeros(48, dtype=torch.complex128, device="cuda"))
+
+
+FIG2 = [(a, M, lam2) for a, M in [(32, 64), (40, 60), (60, 80)] for lam2 in (1, 2, 3, 5, 7, 10)]
+
+
+@pytest.mark.parametrize("a,M,lam2", FIG2)
+def test_fig2_grid_sampled(torch_cuda, nsdgt, oracle_mod, a, M, lam2):
+    """The Fig. 2 lattices (L = lcm(a, M) 2520, lambda = 1/lambda2) that
+    tools/fig2_sweep.py times: one signal, sampled columns against the oracle (c64)."""
+    torch = torch_cuda
+    L = a * M // math.gcd(a, M) * 2520
+    lam1 = 0 if lam2 == 1 else 1
+    g = pgauss_c(L, a * M / L)
+    f, _ = random_pair(L, 60 + lam2, dtype="c64")
+    plan = nsdgt.Plan(L, a, M, lam1, lam2, g, dtype="c64")
+    c = plan.execute(torch.from_numpy(f).cuda())
+    cols = np.sort(np.random.default_rng(lam2).choice(L // a, 12, replace=False))
+    ref = oracle_mod.dgt(f, g, a, M, lam1, lam2, cols=cols)
+    assert rel(c[:, torch.from_numpy(cols).cuda()].cpu().numpy(), ref) <= TOL["c64"], plan.info
+
+
+def pgauss_c(L, tfr):
+    from synthetic import pgauss
+    return pgauss(L, tfr).astype(np.complex64)
