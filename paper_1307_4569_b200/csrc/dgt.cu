@@ -761,6 +761,152 @@ __global__ void __launch_bounds__(256) out_adj_kernel(OutArgs A) {
     }
 }
 
+// Adjoints of the config-4 kernels (same CTA shapes and passes, run backwards).
+// F-branch remap gather for column m: put(i, E(k,m) conj(c[kt][mt])) for kc = kc0 + 256 i
+// (the conjugated X' = conj(E) c of the adjoint remap), residues advanced as in fb_column.
+template <int CNT, typename C, class Put>
+__device__ __forceinline__ void fb_gather(const OutArgs& A, const C* cin, unsigned long long m, unsigned int kc0,
+                                          Put&& put) {
+    const FbCol cc = fb_col(A, m);
+    const unsigned int Nn = (unsigned int)A.N, twoN = 2 * Nn, bu = (unsigned int)A.b;
+    FbIter<C> it = fb_iter<C>(A, cc, kc0 ? (unsigned long long)A.Nr - kc0 : 0ull);
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+        if (i == 1 && kc0 == 0) it = fb_iter<C>(A, cc, (unsigned long long)A.Nr - 256u);
+        else if (i > 0) fb_step(A, it);
+        C ph;
+        if (A.C3) {
+            const unsigned int s2 = bmod((unsigned long long)it.sq * it.sq, twoN, A.inv2N);
+            const unsigned int t1 = bmod((unsigned long long)A.C3 * s2, twoN, A.inv2N);
+            ph = __ldg((const C*)A.ptab + submod(t1, it.t2, twoN));
+        } else {
+            ph = it.ph;
+        }
+        const unsigned int mt = it.sq >= Nn ? it.sq - Nn : it.sq;
+        unsigned int kt = __umulhi(it.xx, A.invb);
+        unsigned int r = it.xx - kt * bu;
+        if (r >= bu) { r -= bu; ++kt; }
+        if (r >= bu) ++kt;
+        const C v = cin[(size_t)kt * Nn + mt];
+        put(i, cmul(ph, mk<decltype(v.x)>(v.x, -v.y)));
+    }
+}
+
+// Adjoint of out_f4096_kernel: c -> C[w][j][kappa][n'] for N_r = iM = 4096.  Thread t gathers
+// conj(X'(t + 256 r)) (the pass-1 input layout), the three radix-16 passes run as in the
+// forward kernel, and pass 3's outputs X(j) give C'(j) = conj(X(j)).
+template <typename T, int MINB>
+__global__ void __launch_bounds__(256, MINB) out_f4096_adj_kernel(OutArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using C = cx<T>;
+    C* S = (C*)smem_raw;
+    const int tid = threadIdx.x;
+    const int m = blockIdx.x;
+    const int64_t w = blockIdx.y;
+    const int qi = (int)A.q, di = (int)A.d;
+    const C* __restrict__ tw = (const C*)A.tw;
+    const C* cin = (const C*)A.out + w * A.M * A.N;
+    C v[16];
+    fb_gather<16>(A, cin, (unsigned long long)m, (unsigned int)tid, [&](int i, C x) { v[i] = x; });
+    dft16<T>(v);
+    twiddle15(v, tw, tid);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) S[k * 256 + tid] = v[k];
+    __syncthreads();
+    const int hi = tid >> 4, lo = tid & 15;
+#pragma unroll
+    for (int t2 = 0; t2 < 16; ++t2) v[t2] = S[hi * 256 + lo + 16 * t2];
+    __syncthreads();
+    dft16<T>(v);
+    twiddle15(v, tw, 16 * lo);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) S[hi * 272 + 17 * k + lo] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int t1 = 0; t1 < 16; ++t1) v[t1] = S[hi * 272 + 17 * lo + t1];
+    dft16<T>(v);
+    C* dst = (C*)A.C + w * A.iM * A.iN + (m % qi) * di + m / qi;
+    const int ld = qi * di;
+#pragma unroll
+    for (int k3 = 0; k3 < 16; ++k3) dst[(hi + 16 * lo + 256 * k3) * ld] = mk<T>(v[k3].x, -v[k3].y);
+}
+
+// Adjoint of zak_ct_kernel (d = D, q = Q, RBC columns): gather conj(T'_u(tau)) for all u
+// through the inverse scatter map, one DFT_D of Q RBC sequences, conj(Phi')(nu) =
+// sum_u Y_u(nu) G_u(nu), one DFT_D of the RBC columns, f(x) = conj(chirp(x) R(s)).
+template <typename T, int D, int Q, int RBC>
+__global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fout) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using C = cx<T>;
+    constexpr int NT = 256, NG = (RBC * D + NT - 1) / NT, NP = (Q * RBC * D + NT - 1) / NT;
+    const int c = (int)A.c;
+    const int nrb = c / RBC;
+    const int rblk = blockIdx.x % nrb, l = blockIdx.x / nrb;
+    const int64_t w = blockIdx.y;
+    const int r0 = rblk * RBC;
+    C* R1 = (C*)smem_raw;
+    C* R2 = R1 + Q * RBC * D;
+    const C* __restrict__ tw = (const C*)A.tw;
+    const int tid = threadIdx.x;
+    {
+        const C* Cw = (const C*)A.C + w * A.iM * Q * D;
+        const int jbase = r0 + c * (l % Q);
+        C v[NP];
+#pragma unroll
+        for (int it = 0; it < NP; ++it) {
+            const int i = tid + it * NT;
+            if (i < Q * RBC * D) {
+                const int u = i / (RBC * D), rem = i % (RBC * D);
+                const int rr = rem / D, np = rem % D;
+                v[it] = Cw[((jbase + rr) * Q + (l - u + Q) % Q) * D + np];
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < NP; ++it) {
+            const int i = tid + it * NT;
+            if (i < Q * RBC * D) {
+                const int u = i / (RBC * D), rem = i % (RBC * D);
+                const int rr = rem / D, np = rem % D;
+                int tau = D - np - (l < u ? 1 : 0);
+                if (tau >= D) tau -= D;
+                R1[(u * RBC + rr) * D + tau] = mk<T>(v[it].x, -v[it].y);
+            }
+        }
+    }
+    __syncthreads();
+    C* Y = fft_ct<T, D>(R1, R2, Q * RBC, tw);   // in R1
+    {
+        const C* __restrict__ G = (const C*)A.G;
+#pragma unroll
+        for (int it = 0; it < NG; ++it) {
+            const int i = tid + it * NT;
+            if (i < RBC * D) {
+                const int rr = i / D, nu = i % D;
+                C acc = cmul(Y[rr * D + nu], __ldg(G + ((r0 + rr) * Q) * D + nu));
+#pragma unroll
+                for (int u = 1; u < Q; ++u)
+                    acc = acc + cmul(Y[(u * RBC + rr) * D + nu], __ldg(G + ((r0 + rr) * Q + u) * D + nu));
+                R2[i] = acc;
+            }
+        }
+    }
+    __syncthreads();
+    C* R = fft_ct<T, D>(R2, R1 + Q * RBC * D - RBC * D, RBC, tw);   // scratch: the tail of R1 (Y is dead)
+    const C* __restrict__ chirp = (const C*)A.chirp;
+    C* fo = (C*)fout + w * A.L;
+#pragma unroll
+    for (int it = 0; it < NG; ++it) {
+        const int i = tid + it * NT;
+        if (i < RBC * D) {
+            const int rr = i % RBC, s = i / RBC;   // rr fastest: RBC consecutive residues per row s
+            const int x = r0 + rr + c * (l + Q * s);
+            C v = R[rr * D + s];
+            if (chirp) v = cmul(v, __ldg(chirp + x));
+            fo[x] = mk<T>(v.x, -v.y);
+        }
+    }
+}
+
 // Adjoint of zak_kernel: C[w][j][kappa][n'] -> f~[w][x].  Same CTA tiling (signal, residue
 // block, l).  Per u: gather T'(tau) (the scatter read backwards), adjoint DFT_d over tau,
 // accumulate Phi'(k; nu) += Y'_u(nu) conj(G(k, u; nu)); then the adjoint DFT_d over nu and the
@@ -1327,6 +1473,14 @@ static int configure(Plan* P, int64_t max_chunk) {
     P->smemAinv = (size_t)P->RB * (2 * I.p + 1) * I.d * e;
     CUDA_TRY(cudaFuncSetAttribute(zak_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemAinv));
     CUDA_TRY(cudaFuncSetAttribute(out_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
+    if (P->zct) {
+        CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+        CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+    }
+    CUDA_TRY(cudaFuncSetAttribute(out_f4096_adj_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kOutF4096Elems * e)));
+    CUDA_TRY(cudaFuncSetAttribute(out_f4096_adj_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kOutF4096Elems * e)));
     // chunk: intermediate of a chunk stays well inside L2
     const size_t per_sig = (size_t)I.iM * I.iN * e;
     int64_t ch = std::max<int64_t>(1, (int64_t)((size_t)(l2 > 0 ? l2 : (64 << 20)) * 2 / 5 / per_sig));
@@ -1355,7 +1509,7 @@ static int alloc_workspace(Plan* P, int64_t Wc) {
 
 // Synthesis of Wc signals: c (device, Wc x M x N) -> f (device, Wc x L complex).
 template <typename T>
-static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cudaStream_t st) {
+static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cudaStream_t st, void* spectra) {
     using C = cx<T>;
     const dgt_lattice_info& I = P->info;
     const double e = (double)sizeof(C), L = (double)I.L, MN = (double)I.M * (double)I.N;
@@ -1380,7 +1534,12 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     B.invL = ~0ull / (unsigned long long)I.L;
     const int ntiles = B.grouped ? (int)(I.q * ((I.d + P->NT - 1) / P->NT)) : (int)((I.iN + P->NT - 1) / P->NT);
     int ph = prof_open(P, st);
-    out_adj_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
+    if (P->outk == 2)
+        out_f4096_adj_kernel<T, 2><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+    else if (P->outk == 1)
+        out_f4096_adj_kernel<T, 3><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+    else
+        out_adj_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
     prof_close(P, ph, PK_OUTADJ, Wc * MN * e, Wc * (4.0 * MN * std::log2((double)I.iM) + 6.0 * MN), st);
     ZakArgs A{};
     A.f = nullptr; A.real_in = 0; A.chirp = P->chirp; A.G = P->G; A.C = P->Cinv;
@@ -1388,26 +1547,39 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = 0;
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     const bool freq = I.branch == DGT_BRANCH_FREQ;
-    void* zout = freq ? P->finv : f;
+    void* zout = freq ? spectra : f;
     const double lg_d = std::log2((double)I.d);
     ph = prof_open(P, st);
-    zak_adj_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemAinv, st>>>(A, zout);
+    if (P->zct == 180 && sizeof(C) == 16)
+        zak_ct_adj_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
+    else if (P->zct == 180)
+        zak_ct_adj_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
+    else
+        zak_adj_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemAinv, st>>>(A, zout);
     prof_close(P, ph, PK_ZAKADJ, Wc * L * e + L * e, Wc * (8.0 * L * I.q / I.p + 4.0 * L * lg_d + 4.0 * MN * lg_d), st);
-    if (freq) {
-        // adjoint of f^ = fft(pchirp(L, s1) f): unnormalised inverse FFT, then conj(pchirp)
-        ph = prof_open(P, st);
-        cufftHandle h;
-        int rc = get_fft_plan(P, Wc, st, &h);
-        if (rc) return rc;
-        void* dst = P->pre ? P->finv : f;
-        if (P->dtype == DGT_C64)
-            CUFFT_TRY(cufftExecC2C(h, (cufftComplex*)P->finv, (cufftComplex*)dst, CUFFT_INVERSE));
-        else
-            CUFFT_TRY(cufftExecZ2Z(h, (cufftDoubleComplex*)P->finv, (cufftDoubleComplex*)dst, CUFFT_INVERSE));
-        if (P->pre)
-            k_conj_chirp<T><<<grid_for(Wc * I.L), 256, 0, st>>>((C*)f, (const C*)P->finv, (const C*)P->pre, I.L, Wc * I.L);
-        prof_close(P, ph, PK_FRONT, Wc * L * e, Wc * 4.0 * L * std::log2(L), st);
-    }
+    CUDA_TRY(cudaGetLastError());
+    return DGT_OK;
+}
+
+// F-branch synthesis tail for nb signals: the adjoint of f^ = fft(pchirp(L, s1) f) -- one
+// batched unnormalised inverse FFT of the spectra (P->finv), then conj(pchirp(L, s1)).
+template <typename T>
+static int launch_inverse_tail(Plan* P, void* f, int64_t nb, cudaStream_t st) {
+    using C = cx<T>;
+    const dgt_lattice_info& I = P->info;
+    const double e = (double)sizeof(C), L = (double)I.L;
+    const int ph = prof_open(P, st);
+    cufftHandle h;
+    int rc = get_fft_plan(P, nb, st, &h);
+    if (rc) return rc;
+    void* dst = P->pre ? P->finv : f;
+    if (P->dtype == DGT_C64)
+        CUFFT_TRY(cufftExecC2C(h, (cufftComplex*)P->finv, (cufftComplex*)dst, CUFFT_INVERSE));
+    else
+        CUFFT_TRY(cufftExecZ2Z(h, (cufftDoubleComplex*)P->finv, (cufftDoubleComplex*)dst, CUFFT_INVERSE));
+    if (P->pre)
+        k_conj_chirp<T><<<grid_for(nb * I.L), 256, 0, st>>>((C*)f, (const C*)P->finv, (const C*)P->pre, I.L, nb * I.L);
+    prof_close(P, ph, PK_FRONT, nb * L * e, nb * 4.0 * L * std::log2(L), st);
     CUDA_TRY(cudaGetLastError());
     return DGT_OK;
 }
@@ -1426,17 +1598,32 @@ static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStrea
         CUDA_TRY(cudaGetLastError());
         return DGT_OK;
     }
+    const bool freq = I.branch == DGT_BRANCH_FREQ;
+    // frequency shear: spectra of a batch of ib signals (a multiple of the chunk, ~192 MB) are
+    // collected and inverse-transformed by one batched cuFFT call
+    const int64_t ib = freq ? std::max<int64_t>(1, (int64_t)((192ull << 20) / ((size_t)I.L * P->esz)) / P->inv_chunk) *
+                                  P->inv_chunk
+                            : W;
     if (!P->Cinv) {
         CUDA_TRY(cudaMalloc(&P->Cinv, (size_t)P->inv_chunk * I.iM * I.iN * P->esz));
-        if (I.branch == DGT_BRANCH_FREQ) CUDA_TRY(cudaMalloc(&P->finv, (size_t)P->inv_chunk * I.L * P->esz));
+        if (freq) CUDA_TRY(cudaMalloc(&P->finv, (size_t)ib * I.L * P->esz));
     }
-    for (int64_t w0 = 0; w0 < W; w0 += P->inv_chunk) {
-        const int64_t wc = std::min<int64_t>(P->inv_chunk, W - w0);
-        const void* cc = (const char*)c + (size_t)w0 * I.M * I.N * P->esz;
-        void* fc = (char*)f + (size_t)w0 * I.L * P->esz;
-        int rc = P->dtype == DGT_C64 ? launch_inverse_chunk<float>(P, cc, fc, wc, st)
-                                     : launch_inverse_chunk<double>(P, cc, fc, wc, st);
-        if (rc) return rc;
+    for (int64_t b0 = 0; b0 < W; b0 += ib) {
+        const int64_t nb = std::min<int64_t>(ib, W - b0);
+        for (int64_t w0 = b0; w0 < b0 + nb; w0 += P->inv_chunk) {
+            const int64_t wc = std::min<int64_t>(P->inv_chunk, b0 + nb - w0);
+            const void* cc = (const char*)c + (size_t)w0 * I.M * I.N * P->esz;
+            void* fc = (char*)f + (size_t)w0 * I.L * P->esz;
+            void* sp = freq ? (void*)((char*)P->finv + (size_t)(w0 - b0) * I.L * P->esz) : nullptr;
+            int rc = P->dtype == DGT_C64 ? launch_inverse_chunk<float>(P, cc, fc, wc, st, sp)
+                                         : launch_inverse_chunk<double>(P, cc, fc, wc, st, sp);
+            if (rc) return rc;
+        }
+        if (freq) {
+            void* fb = (char*)f + (size_t)b0 * I.L * P->esz;
+            int rc = P->dtype == DGT_C64 ? launch_inverse_tail<float>(P, fb, nb, st) : launch_inverse_tail<double>(P, fb, nb, st);
+            if (rc) return rc;
+        }
     }
     return DGT_OK;
 }

@@ -157,3 +157,21 @@ def test_fused_synthesis_matches_generic_and_oracle(torch_cuda, nsdgt, oracle_mo
     assert rel(ff, fg) <= TOL["c64"]
     ref = oracle_mod.idgt(c[W - 1].astype(np.complex128), g, wl.a, wl.M, wl.lam1, wl.lam2)
     assert rel(ff[W - 1], ref) <= TOL["c64"]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_config4_synthesis_kernels_match_generic(torch_cuda, nsdgt, dtype, monkeypatch):
+    """Config 4's synthesis kernels (zak_ct_adj_kernel, out_f4096_adj_kernel) against the generic
+    adjoint kernels (selected at plan time by NSDGT_ZAK_RT / NSDGT_OUT_GENERIC)."""
+    torch = torch_cuda
+    wl = CONFIGS[3]
+    g = window(wl)
+    rng = np.random.default_rng(12)
+    c = torch.from_numpy(rand_c(rng, 2, wl.M, wl.N, dtype)).cuda()
+    pf = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
+    ff = pf.inverse(c).cpu().numpy()
+    monkeypatch.setenv("NSDGT_ZAK_RT", "1")
+    monkeypatch.setenv("NSDGT_OUT_GENERIC", "1")
+    pg = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
+    fg = pg.inverse(c).cpu().numpy()
+    assert rel(ff, fg) <= TOL[dtype]
