@@ -200,6 +200,8 @@ struct ZakArgs {
     int64_t L, c, d, p, q, iM;
     int RB;
     int allu;           // p = 1: products and DFT_d of all q values of u in one pass (smem 2 q RB d)
+    unsigned char* gscr;   // non-null: per-CTA buffers in global memory (d too large for shared)
+    int64_t gstride;       // bytes per CTA in gscr
     Radices rd;
     const void* tw;     // twiddles of length d
 };
@@ -216,7 +218,8 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
     const int64_t w = blockIdx.y;
     const int64_t r0 = (int64_t)rblk * RB;
     const int nr = (int)((c - r0) < RB ? (c - r0) : RB);
-    C* bufA = (C*)smem_raw;                 // RB*p*d
+    unsigned char* sbase = A.gscr ? A.gscr + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * A.gstride : smem_raw;
+    C* bufA = (C*)sbase;                    // RB*p*d
     C* bufB = bufA + (size_t)RB * p * d;    // RB*p*d (>= RB*d)
     C* bufY = bufB + (size_t)RB * p * d;    // RB*d
     const C* __restrict__ tw = (const C*)A.tw;
@@ -405,6 +408,8 @@ struct OutArgs {
     void* out;      // [W][M][N]
     int64_t iM, iN, q, d;
     int NT;         // columns per CTA: T-branch consecutive inner n; F-branch (grouped) n = kappa + q (n'0 + i)
+    unsigned char* gscr;   // non-null: per-CTA buffers in global memory (iM too large for shared)
+    int64_t gstride;
     int grouped;    // 1: CTA x = (kappa, block of NT consecutive n'), contiguous loads
     Radices rd;
     const void* tw;  // twiddles of length iM
@@ -554,7 +559,8 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
         nt = (int)((iN - nb) < NT ? (iN - nb) : NT);
     }
     const int64_t w = blockIdx.y;
-    C* bufA = (C*)smem_raw;
+    unsigned char* sbase = A.gscr ? A.gscr + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * A.gstride : smem_raw;
+    C* bufA = (C*)sbase;
     C* bufB = bufA + (size_t)NT * iM;
     const C* __restrict__ Cin = (const C*)A.C + w * iM * iN;
     // load columns: C(j, n) stored at [j][n mod q][n div q] (32-bit indices within a signal);
@@ -701,7 +707,8 @@ __global__ void __launch_bounds__(256) out_adj_kernel(OutArgs A) {
         nt = (int)((iN - nb) < NT ? (iN - nb) : NT);
     }
     const int64_t w = blockIdx.y;
-    C* bufA = (C*)smem_raw;
+    unsigned char* sbase = A.gscr ? A.gscr + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * A.gstride : smem_raw;
+    C* bufA = (C*)sbase;
     C* bufB = bufA + (size_t)NT * iM;
     const C* cin = (const C*)A.out + w * A.M * A.N;   // the coefficients (input here)
     // bufA = conj(X'), the input of the forward engine
@@ -924,7 +931,8 @@ __global__ void __launch_bounds__(256) zak_adj_kernel(ZakArgs A, void* fout) {
     const int64_t w = blockIdx.y;
     const int64_t r0 = (int64_t)rblk * RB;
     const int nr = (int)((c - r0) < RB ? (c - r0) : RB);
-    C* acc = (C*)smem_raw;                  // RB*p*d: conj(Phi')
+    unsigned char* sbase = A.gscr ? A.gscr + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * A.gstride : smem_raw;
+    C* acc = (C*)sbase;                     // RB*p*d: conj(Phi')
     C* bufB = acc + (size_t)RB * p * d;     // RB*p*d
     C* bufY = bufB + (size_t)RB * p * d;    // RB*d
     const C* __restrict__ tw = (const C*)A.tw;
@@ -1148,6 +1156,9 @@ struct Plan {
     int RB = 1, NT = 1;
     size_t smemA = 0, smemB = 0;
     int allu = 0;            // zak_kernel all-u mode (p = 1)
+    int gA = 0, gB = 0;      // Zak / output kernels with per-CTA buffers in global scratch
+    unsigned char* scrA = nullptr;
+    unsigned char* scrB = nullptr;
     // synthesis (dgt_execute_inverse): chunk, zak_adj_kernel smem, workspace (allocated on
     // first use: C intermediate + F-branch spectra)
     int64_t inv_chunk = 1;
@@ -1212,7 +1223,8 @@ static void prof_close(Plan* P, int h, int kind, double bytes, double flops, cud
 static void free_plan(Plan* P) {
     if (!P) return;
     void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
-                    P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv, P->gt64};
+                    P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv, P->gt64,
+                    P->scrA, P->scrB};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     free_fast(&P->fp);
@@ -1369,6 +1381,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     A.f = src; A.real_in = real_src; A.chirp = P->chirp; A.G = P->G; A.C = P->Cws;
     A.L = I.L; A.c = I.c; A.d = I.d; A.p = I.p; A.q = I.q; A.iM = I.iM;
     A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = P->allu;
+    A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
     if (P->zct == 180 && sizeof(C) == 16)
@@ -1376,11 +1389,12 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     else if (P->zct == 180)
         zak_ct_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     else
-        zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+        zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->gA ? 0 : P->smemA, st>>>(A);
     prof_close(P, ph, P->zct ? PK_ZAKCT : PK_ZAK, by_in, fl_zak, st);
     OutArgs B{};
     B.C = P->Cws; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
     B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
+    B.gscr = P->gB ? P->scrB : nullptr; B.gstride = (int64_t)P->smemB;
     B.grouped = I.branch == DGT_BRANCH_FREQ ? 1 : 0;
     B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
     B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
@@ -1404,7 +1418,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     else if (P->outk == 2)
         out_f4096_kernel<T, 2><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
     else
-        out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
+        out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->gB ? 0 : P->smemB, st>>>(B);
     prof_close(P, ph, P->outk ? PK_OUTF : PK_OUT, by_out, fl_out, st);
     CUDA_TRY(cudaGetLastError());
     return DGT_OK;
@@ -1431,8 +1445,9 @@ static int configure(Plan* P, int64_t max_chunk) {
     auto smemA = [&](int rb) { return (size_t)rb * (2 * I.p + 1) * I.d * e; };
     int rb = (int)std::min<int64_t>(I.c, std::max<int64_t>(1, 64 / (int64_t)e));
     while (rb > 1 && smemA(rb) > budget) --rb;
-    if (smemA(rb) > budget)
-        return fail(DGT_EUNSUPPORTED, "inner Zak length d=" + std::to_string(I.d) + " too large for shared memory");
+    // d too large for shared memory: the Zak kernels keep their buffers in a per-CTA global
+    // scratch (L2-resident; correct, slower)
+    P->gA = smemA(rb) > budget ? 1 : 0;
     P->RB = rb;
     P->smemA = smemA(rb);
     // p = 1: all-u mode when two regions of q RB d fit (config 4: 92 KB, 2 CTAs per SM)
@@ -1448,11 +1463,10 @@ static int configure(Plan* P, int64_t max_chunk) {
     while (nt > 1 && smemB(nt) > budget / 2 && smemB(nt) > 48 * 1024) --nt;
     if (const char* ev = std::getenv("NSDGT_OUT_NT")) nt = std::max(1, std::atoi(ev));   // experiment
     while (nt > 1 && smemB(nt) > budget) --nt;
-    if (smemB(nt) > budget)
-        return fail(DGT_EUNSUPPORTED, "inner channel count " + std::to_string(I.iM) + " too large for shared memory");
+    P->gB = smemB(nt) > budget ? 1 : 0;   // likewise for the output kernels
     P->NT = nt;
     P->smemB = smemB(nt);
-    CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+    CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gA ? 0 : (int)P->smemA));
     // compile-time Zak kernel: d = 180, q = 4, p = 1, RB = 64 / e columns dividing c
     P->zct = (P->allu && I.d == 180 && I.q == 4 && I.c % P->RB == 0 && P->RB == (int)(64 / e) &&
               !std::getenv("NSDGT_ZAK_RT")) ? 180 : 0;
@@ -1460,7 +1474,7 @@ static int configure(Plan* P, int64_t max_chunk) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
     }
-    CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
+    CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     // out_f4096: 2 CTAs per SM for c128 (128 registers, measured faster than 3 CTAs at 80
     // registers with spills), 3 for c64
     P->outk = (I.branch == DGT_BRANCH_FREQ && I.iM == 4096 && !std::getenv("NSDGT_OUT_GENERIC")) ? (e == 16 ? 2 : 1) : 0;
@@ -1471,8 +1485,8 @@ static int configure(Plan* P, int64_t max_chunk) {
                                   (int)(kOutF4096Elems * e)));
     // synthesis kernels (the adjoints of zak_kernel / out_kernel)
     P->smemAinv = (size_t)P->RB * (2 * I.p + 1) * I.d * e;
-    CUDA_TRY(cudaFuncSetAttribute(zak_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemAinv));
-    CUDA_TRY(cudaFuncSetAttribute(out_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
+    CUDA_TRY(cudaFuncSetAttribute(zak_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gA ? 0 : (int)P->smemAinv));
+    CUDA_TRY(cudaFuncSetAttribute(out_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     if (P->zct) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
@@ -1493,6 +1507,16 @@ static int configure(Plan* P, int64_t max_chunk) {
 static int alloc_workspace(Plan* P, int64_t Wc) {
     const dgt_lattice_info& I = P->info;
     if (P->Cws) return DGT_OK;
+    // global per-CTA scratch of the Zak / output kernels when their buffers exceed shared memory
+    const int64_t wmax = std::max<int64_t>(Wc, P->inv_chunk);
+    if (P->gA) {
+        const int64_t ctas = ((I.c + P->RB - 1) / P->RB) * I.q * wmax;
+        CUDA_TRY(cudaMalloc(&P->scrA, (size_t)ctas * std::max(P->smemA, P->smemAinv)));
+    }
+    if (P->gB) {
+        const int64_t tiles = (I.branch == DGT_BRANCH_FREQ ? I.q * ((I.d + P->NT - 1) / P->NT) : (I.iN + P->NT - 1) / P->NT);
+        CUDA_TRY(cudaMalloc(&P->scrB, (size_t)tiles * wmax * P->smemB));
+    }
     size_t need = P->fast ? fast_workspace_bytes(&P->fp, Wc) : (size_t)Wc * I.iM * I.iN * P->esz;
     CUDA_TRY(cudaMalloc(&P->Cws, need));
     P->ws_bytes = need;
@@ -1516,6 +1540,7 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     OutArgs B{};
     B.C = P->Cinv; B.out = const_cast<void*>(c); B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
     B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
+    B.gscr = P->gB ? P->scrB : nullptr; B.gstride = (int64_t)P->smemB;
     B.grouped = I.branch == DGT_BRANCH_FREQ ? 1 : 0;
     B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
     B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
@@ -1539,12 +1564,13 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     else if (P->outk == 1)
         out_f4096_adj_kernel<T, 3><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
     else
-        out_adj_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
+        out_adj_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->gB ? 0 : P->smemB, st>>>(B);
     prof_close(P, ph, PK_OUTADJ, Wc * MN * e, Wc * (4.0 * MN * std::log2((double)I.iM) + 6.0 * MN), st);
     ZakArgs A{};
     A.f = nullptr; A.real_in = 0; A.chirp = P->chirp; A.G = P->G; A.C = P->Cinv;
     A.L = I.L; A.c = I.c; A.d = I.d; A.p = I.p; A.q = I.q; A.iM = I.iM;
     A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = 0;
+    A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     const bool freq = I.branch == DGT_BRANCH_FREQ;
     void* zout = freq ? spectra : f;
@@ -1555,7 +1581,7 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     else if (P->zct == 180)
         zak_ct_adj_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
     else
-        zak_adj_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemAinv, st>>>(A, zout);
+        zak_adj_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->gA ? 0 : P->smemAinv, st>>>(A, zout);
     prof_close(P, ph, PK_ZAKADJ, Wc * L * e + L * e, Wc * (8.0 * L * I.q / I.p + 4.0 * L * lg_d + 4.0 * MN * lg_d), st);
     CUDA_TRY(cudaGetLastError());
     return DGT_OK;

@@ -290,3 +290,24 @@ def test_fig2_grid_sampled(torch_cuda, nsdgt, oracle_mod, a, M, lam2):
 def pgauss_c(L, tfr):
     from synthetic import pgauss
     return pgauss(L, tfr).astype(np.complex64)
+
+
+@pytest.mark.parametrize("lam2", [1, 2])
+def test_large_inner_length_global_scratch(torch_cuda, nsdgt, oracle_mod, lam2):
+    """Fig. 2 lattice (60, 80) in complex128 with a time shear / separable: the inner Zak length
+    d = 2520 needs 7 d 16 B of buffers per CTA, beyond shared memory, so the Zak kernels run on
+    per-CTA global scratch.  Forward on sampled columns and synthesis of one signal."""
+    torch = torch_cuda
+    a, M = 60, 80
+    L = a * M // math.gcd(a, M) * 2520
+    lam1 = 0 if lam2 == 1 else 1
+    f, g = random_pair(L, 70 + lam2, dtype="c128")
+    plan = nsdgt.Plan(L, a, M, lam1, lam2, g, dtype="c128")
+    assert plan.info["d"] == 2520
+    c = plan.execute(torch.from_numpy(f).cuda())
+    cols = np.sort(np.random.default_rng(lam2).choice(L // a, 8, replace=False))
+    ref = oracle_mod.dgt(f, g, a, M, lam1, lam2, cols=cols)
+    assert rel(c[:, torch.from_numpy(cols).cuda()].cpu().numpy(), ref) <= TOL["c128"]
+    cr = np.random.default_rng(5).standard_normal((M, L // a)) + 0j
+    fi = plan.inverse(torch.from_numpy(cr).cuda()).cpu().numpy()
+    assert rel(fi, oracle_mod.idgt(cr, g, a, M, lam1, lam2)) <= TOL["c128"]
