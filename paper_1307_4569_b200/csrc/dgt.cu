@@ -1149,6 +1149,7 @@ struct Plan {
     void* fhat = nullptr;    // F-branch chunk spectra
     int64_t chunk = 1;
     int64_t fb = 1;          // F-branch front batch (signals per cuFFT call)
+    int64_t ib = 1;          // F-branch synthesis batch
     size_t ws_bytes = 0;
     std::map<int64_t, cufftHandle> fft_plans;
     // kernel configuration
@@ -1262,6 +1263,34 @@ static int get_fft_plan(Plan* P, int64_t batch, cudaStream_t st, cufftHandle* ou
     return DGT_OK;
 }
 
+// Length-L FFTs of nb signals (in -> out, may alias) with the plans made at plan time: one
+// call when a plan for this batch exists (the front / synthesis batch), else nb calls of the
+// batch-1 plan -- so dgt_execute never creates a cuFFT plan (no allocation in execute).
+static int exec_fft(Plan* P, const void* in, void* out, int64_t nb, int dir, cudaStream_t st) {
+    const size_t per = (size_t)P->info.L * P->esz;
+    auto run = [&](cufftHandle h, const void* a, void* b) -> cufftResult {
+        cufftSetStream(h, st);
+        return P->dtype == DGT_C64 ? cufftExecC2C(h, (cufftComplex*)a, (cufftComplex*)b, dir)
+                                   : cufftExecZ2Z(h, (cufftDoubleComplex*)a, (cufftDoubleComplex*)b, dir);
+    };
+    // the largest planned batch <= the signals left, repeatedly (plans exist for the front and
+    // synthesis batches and every power of two below them)
+    int64_t done = 0;
+    while (done < nb) {
+        auto it = P->fft_plans.upper_bound(nb - done);
+        if (it == P->fft_plans.begin()) {   // no plan at all (not expected): make the batch-1 plan
+            cufftHandle h1;
+            int rc = get_fft_plan(P, 1, st, &h1);
+            if (rc) return rc;
+            continue;
+        }
+        --it;
+        CUFFT_TRY(run(it->second, (const char*)in + done * per, (char*)out + done * per));
+        done += it->first;
+    }
+    return DGT_OK;
+}
+
 template <typename T>
 static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st) {
     using C = cx<T>;
@@ -1331,19 +1360,14 @@ static int launch_front(Plan* P, const void* f, int64_t nb, cudaStream_t st) {
     const bool real_in = (P->flags & DGT_REAL_INPUT) != 0;
     const double e = (double)sizeof(C), ein = real_in ? e / 2 : e, L = (double)I.L;
     const int ph = prof_open(P, st);
-    cufftHandle h;
-    int rc = get_fft_plan(P, nb, st, &h);
-    if (rc) return rc;
     const void* fin = f;
     if (real_in || P->pre) {
         k_prechirp<T><<<grid_for(nb * I.L), 256, 0, st>>>((C*)P->fhat, f, real_in ? 1 : 0, (const C*)P->pre, I.L,
                                                           nb * I.L);
         fin = P->fhat;
     }
-    if (P->dtype == DGT_C64)
-        CUFFT_TRY(cufftExecC2C(h, (cufftComplex*)fin, (cufftComplex*)P->fhat, CUFFT_FORWARD));
-    else
-        CUFFT_TRY(cufftExecZ2Z(h, (cufftDoubleComplex*)fin, (cufftDoubleComplex*)P->fhat, CUFFT_FORWARD));
+    int rc = exec_fft(P, fin, P->fhat, nb, CUFFT_FORWARD, st);
+    if (rc) return rc;
     // Table 1 "Freq. shear": one length-L FFT of f per signal (4 L log2 L)
     prof_close(P, ph, PK_FRONT, nb * L * ein, nb * 4.0 * L * std::log2(L), st);
     CUDA_TRY(cudaGetLastError());
@@ -1527,6 +1551,16 @@ static int alloc_workspace(Plan* P, int64_t Wc) {
         P->fb = std::max<int64_t>(1, want / Wc) * Wc;
         CUDA_TRY(cudaMalloc(&P->fhat, (size_t)P->fb * per));
         P->ws_bytes += (size_t)P->fb * per;
+        // the cuFFT plans execute uses: the front and synthesis batches and the powers of two
+        // below them (ragged batches run as a few batched calls; no plan is made in execute)
+        P->ib = std::max<int64_t>(1, want / P->inv_chunk) * P->inv_chunk;
+        std::vector<int64_t> sizes = {P->fb, P->ib};
+        for (int64_t b = 1; b < std::max(P->fb, P->ib); b *= 2) sizes.push_back(b);
+        for (int64_t b : sizes) {
+            cufftHandle h;
+            int rc = get_fft_plan(P, b, nullptr, &h);
+            if (rc) return rc;
+        }
     }
     return DGT_OK;
 }
@@ -1595,14 +1629,9 @@ static int launch_inverse_tail(Plan* P, void* f, int64_t nb, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
     const double e = (double)sizeof(C), L = (double)I.L;
     const int ph = prof_open(P, st);
-    cufftHandle h;
-    int rc = get_fft_plan(P, nb, st, &h);
-    if (rc) return rc;
     void* dst = P->pre ? P->finv : f;
-    if (P->dtype == DGT_C64)
-        CUFFT_TRY(cufftExecC2C(h, (cufftComplex*)P->finv, (cufftComplex*)dst, CUFFT_INVERSE));
-    else
-        CUFFT_TRY(cufftExecZ2Z(h, (cufftDoubleComplex*)P->finv, (cufftDoubleComplex*)dst, CUFFT_INVERSE));
+    int rc = exec_fft(P, P->finv, dst, nb, CUFFT_INVERSE, st);
+    if (rc) return rc;
     if (P->pre)
         k_conj_chirp<T><<<grid_for(nb * I.L), 256, 0, st>>>((C*)f, (const C*)P->finv, (const C*)P->pre, I.L, nb * I.L);
     prof_close(P, ph, PK_FRONT, nb * L * e, nb * 4.0 * L * std::log2(L), st);
@@ -1627,9 +1656,7 @@ static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStrea
     const bool freq = I.branch == DGT_BRANCH_FREQ;
     // frequency shear: spectra of a batch of ib signals (a multiple of the chunk, ~192 MB) are
     // collected and inverse-transformed by one batched cuFFT call
-    const int64_t ib = freq ? std::max<int64_t>(1, (int64_t)((192ull << 20) / ((size_t)I.L * P->esz)) / P->inv_chunk) *
-                                  P->inv_chunk
-                            : W;
+    const int64_t ib = freq ? P->ib : W;
     if (!P->Cinv) {
         CUDA_TRY(cudaMalloc(&P->Cinv, (size_t)P->inv_chunk * I.iM * I.iN * P->esz));
         if (freq) CUDA_TRY(cudaMalloc(&P->finv, (size_t)ib * I.L * P->esz));
