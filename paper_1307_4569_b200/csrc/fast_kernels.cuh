@@ -152,6 +152,8 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     if (std::getenv("NSDGT_VERBOSE"))
         std::fprintf(stderr, "fused7: D=%d CTAs/SM=%d grid=%d smem/CTA=%zu B ring S=%d lag=%d\n", (int)D, per_sm,
                      fp->grid, smem, fp->S, fp->lag);
+    // job queue + per-slot completion counters (allocated here: execute allocates nothing)
+    if (cudaMalloc(&fp->counters, sizeof(int) * (1 + 2 * fp->S)) != cudaSuccess) return DGT_ENOMEM;
     fp->E = E;
     fp->esz = sizeof(float2);
     fp->kind = 2;
@@ -182,9 +184,7 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
     if (real_in || fp->kind != 2) return DGT_EUNSUPPORTED;
     if (W * (int64_t)(fp->nA + fp->nB) >= (int64_t)1 << 31) return DGT_EUNSUPPORTED;   // 32-bit job indices
     const int nctr = 1 + 2 * fp->S;
-    if (!fp->counters) {
-        if (cudaMalloc(&fp->counters, sizeof(int) * nctr) != cudaSuccess) return DGT_ENOMEM;
-    }
+    if (!fp->counters) return DGT_EINVAL;   // allocated by build_fast
     if (cudaMemsetAsync(fp->counters, 0, sizeof(int) * nctr, st) != cudaSuccess) return DGT_ECUDA;
     v7::Args a{};
     a.f = (const float2*)f; a.out = (float2*)c; a.ws = (float2*)ws; a.Gp = (const float4*)fp->Gp;
@@ -210,9 +210,7 @@ inline int launch_fast_adj(FastPlan* fp, const void* c, void* ws, void* f, int64
     if (fp->kind != 2) return DGT_EUNSUPPORTED;
     if (W * (int64_t)(fp->nA + fp->nB) >= (int64_t)1 << 31) return DGT_EUNSUPPORTED;
     const int nctr = 1 + 2 * fp->S;
-    if (!fp->counters) {
-        if (cudaMalloc(&fp->counters, sizeof(int) * nctr) != cudaSuccess) return DGT_ENOMEM;
-    }
+    if (!fp->counters) return DGT_EINVAL;   // allocated by build_fast
     if (cudaMemsetAsync(fp->counters, 0, sizeof(int) * nctr, st) != cudaSuccess) return DGT_ECUDA;
     v7::Args a{};
     a.f = (const float2*)c; a.out = (float2*)f; a.ws = (float2*)ws; a.Gp = (const float4*)fp->Gpa;
