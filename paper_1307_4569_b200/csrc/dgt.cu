@@ -1468,6 +1468,9 @@ static int configure(Plan* P, int64_t max_chunk) {
     // kernel A: residues per CTA for >= 32-byte gathers, within the smem budget
     auto smemA = [&](int rb) { return (size_t)rb * (2 * I.p + 1) * I.d * e; };
     int rb = (int)std::min<int64_t>(I.c, std::max<int64_t>(1, 64 / (int64_t)e));
+    // few residue classes (small c, e.g. config 2: c = 50): fewer residues per CTA so that one
+    // signal still spreads over >= 2 CTAs per SM
+    while (rb > 1 && ((I.c + rb - 1) / rb) * I.q < 2 * 148) --rb;
     while (rb > 1 && smemA(rb) > budget) --rb;
     // d too large for shared memory: the Zak kernels keep their buffers in a per-CTA global
     // scratch (L2-resident; correct, slower)
