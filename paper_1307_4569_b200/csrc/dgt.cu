@@ -1167,6 +1167,7 @@ struct Plan {
     void* Cinv = nullptr;
     void* finv = nullptr;
     int zct = 0;             // zak_kernel compile-time inner length (0 = runtime radices)
+    int inv_generic = 0;     // experiment knob (NSDGT_INV_GENERIC, read at plan time): generic synthesis
     int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
     int fast = 0;  // specialised path id (0 = generic)
     FastPlan fp{};
@@ -1510,6 +1511,7 @@ static int configure(Plan* P, int64_t max_chunk) {
                                   (int)(kOutF4096Elems * e)));
     CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kOutF4096Elems * e)));
+    P->inv_generic = std::getenv("NSDGT_INV_GENERIC") ? 1 : 0;
     // synthesis kernels (the adjoints of zak_kernel / out_kernel)
     P->smemAinv = (size_t)P->RB * (2 * I.p + 1) * I.d * e;
     CUDA_TRY(cudaFuncSetAttribute(zak_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gA ? 0 : (int)P->smemAinv));
@@ -1644,7 +1646,7 @@ static int launch_inverse_tail(Plan* P, void* f, int64_t nb, cudaStream_t st) {
 
 static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
-    if (P->fast && !std::getenv("NSDGT_INV_GENERIC")) {
+    if (P->fast && !P->inv_generic) {
         // fused synthesis (fused7_adj.cuh) on the forward ring
         const int ph = prof_open(P, st);
         int rc = launch_fast_adj(&P->fp, c, P->Cws, f, W, st);
@@ -1991,6 +1993,14 @@ int dgt_profile_end(dgt_plan_t plan, dgt_kernel_stat* stats, int max_stats, int*
     P->recs.clear();
     P->pool_used = 0;
     return DGT_OK;
+}
+
+// Debugging aid of -DNSDGT_TRACE builds (tools/v7trace.py; not part of include/nsdgt.h): the
+// device buffer of fused7 phase stamps (8 CTAs x 4096 entries) when the plan was made with
+// NSDGT_DBG & 16, else null.
+void* dgt_debug_trace_log(dgt_plan_t plan) {
+    Plan* P = (Plan*)plan;
+    return P ? (void*)P->fp.tracelog : nullptr;
 }
 
 int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W) {

@@ -40,6 +40,9 @@ struct FastPlan {
     void* Gp = nullptr;          // G' (owned)
     void* Gpa = nullptr;         // G' in the adjoint kernel's order (owned)
     size_t smem_adj = 0;
+    int grid_adj = 0, lag_adj = 0;   // synthesis kernel grid and look-ahead
+    int dbg = 0;                 // experiment knobs (NSDGT_DBG, read once at plan time; fused7.cuh)
+    unsigned long long* tracelog = nullptr;   // dbg & 16: per-CTA phase stamps of a -DNSDGT_TRACE build
     int* counters = nullptr;     // job queue + per-slot completion counters (owned)
 };
 
@@ -154,6 +157,25 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
                      fp->grid, smem, fp->S, fp->lag);
     // job queue + per-slot completion counters (allocated here: execute allocates nothing)
     if (cudaMalloc(&fp->counters, sizeof(int) * (1 + 2 * fp->S)) != cudaSuccess) return DGT_ENOMEM;
+    // Synthesis (fused7_adj.cuh): B' jobs are short (2 tiles) and the long A' jobs (5 tiles)
+    // free the ring slots, so A'(w) needs less lag behind B'(w) than fused7's B behind A, and a
+    // shorter lag leaves more slots between B'(w) and the A'(w - S) it waits for.  Measured:
+    // config 5 lag 2 (S = 8) 6.24 ms against 8.07 ms at fused7's lag 5; config 3 lag 6 (S = 20)
+    // 0.39 ms against 0.48 ms at lag 14.  Its grid: every CTA resident (occupancy query).
+    fp->lag_adj = std::max(1, std::min(fp->S - 1, (2 * fp->lag + 2) / 5));
+    if (const char* e = std::getenv("NSDGT_LAG_ADJ")) fp->lag_adj = std::max(0, std::min(fp->S - 1, std::atoi(e)));
+    {
+        int per_sm_a = 0;
+        const void* ka = D == 512 ? (const void*)v7::fused7a_kernel<512, 3> : (const void*)v7::fused7a_kernel<256, 5>;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, ka, v7::Cfg<512>::NT, fp->smem_adj) != cudaSuccess ||
+            per_sm_a < 1)
+            return DGT_ECUDA;
+        fp->grid_adj = std::min(per_sm * sms, per_sm_a * sms);
+    }
+    fp->dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;   // experiment knobs
+    if (fp->dbg & 16) {   // phase trace of a -DNSDGT_TRACE build (tools/v7trace.py, dgt_debug_trace_log)
+        if (cudaMalloc(&fp->tracelog, sizeof(unsigned long long) * 8 * 4096) != cudaSuccess) return DGT_ENOMEM;
+    }
     fp->E = E;
     fp->esz = sizeof(float2);
     fp->kind = 2;
@@ -162,6 +184,8 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
 }
 
 inline void free_fast(FastPlan* fp) {
+    if (fp->tracelog) cudaFree(fp->tracelog);
+    fp->tracelog = nullptr;
     if (fp->Gp) cudaFree(fp->Gp);
     if (fp->Gpa) cudaFree(fp->Gpa);
     fp->Gpa = nullptr;
@@ -190,13 +214,10 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
     a.f = (const float2*)f; a.out = (float2*)c; a.ws = (float2*)ws; a.Gp = (const float4*)fp->Gp;
     a.E = (const float2*)fp->E; a.ctr = fp->counters; a.W = (int)W; a.N = fp->N; a.c = fp->c; a.Kmod = fp->Kmod;
     a.beta = fp->beta; a.S = fp->S; a.lag = fp->lag; a.nA = fp->nA; a.nB = fp->nB;
-    a.dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;   // experiment knobs (fused7.cuh)
-    if (a.dbg & 16) {   // phase trace of a -DNSDGT_TRACE build (tools/v7trace.py)
-        static unsigned long long* logbuf = nullptr;
-        if (!logbuf) cudaMalloc(&logbuf, sizeof(unsigned long long) * 8 * 4096);
-        cudaMemsetAsync(logbuf, 0, sizeof(unsigned long long) * 8 * 4096, st);
-        a.log = logbuf;
-        if (const char* e = std::getenv("NSDGT_LOGPTR")) *(unsigned long long**)std::strtoull(e, nullptr, 10) = logbuf;
+    a.dbg = fp->dbg;
+    if (fp->tracelog) {
+        cudaMemsetAsync(fp->tracelog, 0, sizeof(unsigned long long) * 8 * 4096, st);
+        a.log = fp->tracelog;
     }
     if (fp->D == 512) (fp->minb == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st);
     else (fp->minb == 5 ? launch7<256, 5> : fp->minb == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st);
@@ -216,25 +237,9 @@ inline int launch_fast_adj(FastPlan* fp, const void* c, void* ws, void* f, int64
     a.f = (const float2*)c; a.out = (float2*)f; a.ws = (float2*)ws; a.Gp = (const float4*)fp->Gpa;
     a.E = (const float2*)fp->E; a.ctr = fp->counters; a.W = (int)W; a.N = fp->N; a.c = fp->c; a.Kmod = fp->Kmod;
     a.beta = fp->beta; a.S = fp->S; a.lag = fp->lag; a.nA = fp->nA; a.nB = fp->nB;
-    // Synthesis look-ahead: B' jobs are short (2 tiles) and the long A' jobs (5 tiles) free the
-    // ring slots, so A'(w) needs less lag behind B'(w) than fused7's B behind A, and a shorter
-    // lag leaves more slots between B'(w) and the A'(w - S) it waits for.  Measured: config 5
-    // lag 2 (S = 8) 6.24 ms against 8.07 ms at fused7's lag 5; config 3 lag 6 (S = 20) 0.39 ms
-    // against 0.48 ms at lag 14.
-    a.lag = std::max(1, std::min(fp->S - 1, (2 * fp->lag + 2) / 5));
-    if (const char* e = std::getenv("NSDGT_LAG_ADJ")) a.lag = std::max(0, std::min(fp->S - 1, std::atoi(e)));   // experiment
-    a.dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;
-    int grid = fp->grid;
-    {
-        int per_sm = 0, dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const void* ka = fp->D == 512 ? (const void*)v7::fused7a_kernel<512, 3> : (const void*)v7::fused7a_kernel<256, 5>;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ka, v7::Cfg<512>::NT, fp->smem_adj) != cudaSuccess ||
-            per_sm < 1)
-            return DGT_ECUDA;
-        grid = std::min(grid, per_sm * sms);   // every CTA of the persistent grid resident
-    }
+    a.lag = fp->lag_adj;
+    a.dbg = fp->dbg;
+    const int grid = fp->grid_adj;
     if (fp->D == 512) launch7a<512, 3>(a, grid, fp->smem_adj, st);
     else launch7a<256, 5>(a, grid, fp->smem_adj, st);
     return DGT_OK;

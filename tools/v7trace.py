@@ -8,12 +8,13 @@ k = int(os.environ.get("CFG", "5")); Wt = int(os.environ.get("WT", "1024"))
 wl = config(k); g = window(wl)
 fb = torch.randn(Wt, wl.L, dtype=torch.complex64, device="cuda")
 cb = torch.empty(Wt, wl.M, wl.N, dtype=torch.complex64, device="cuda")
+os.environ["NSDGT_DBG"] = str(16 | int(os.environ.get("EXTRA", "0")))   # read at plan time
 p = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
 p.execute(fb, out=cb); torch.cuda.synchronize()
-ptr = ctypes.c_uint64(0)
-os.environ["NSDGT_LOGPTR"] = str(ctypes.addressof(ptr))
-os.environ["NSDGT_DBG"] = str(16 | int(os.environ.get("EXTRA", "0")))
-p.execute(fb, out=cb); torch.cuda.synchronize()
+lib = nsdgt.nsdgt._lib
+lib.dgt_debug_trace_log.restype = ctypes.c_void_p
+lib.dgt_debug_trace_log.argtypes = [ctypes.c_void_p]
+ptr = ctypes.c_uint64(lib.dgt_debug_trace_log(p._h) or 0)
 cudart = ctypes.CDLL("libcudart.so") if os.path.exists("/usr/local/cuda/lib64/libcudart.so") else None
 if cudart is None:
     import glob
