@@ -106,6 +106,24 @@ int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t lambda1, 
              const void* g, int dtype, int flags, int64_t max_chunk, int force_shear, int64_t s0,
              int64_t s1, void* cuda_stream);
 
+/* Shear-OLA plan: the DGT on the lattice (a, M,
+ * lambda) of length-L signals with an FIR window g of Lg taps, computed block-wise: blocks of
+ * Lb samples (a multiple of L_min dividing L) are zero-extended to Lx >= Lb + Lg + 2a (a
+ * multiple of L_min with a 7-smooth quotient) and transformed by the shear algorithm
+ * with the window zero-extended to Lx; the block coefficients are overlap-added.  The result is
+ * exactly Eq. (DGT) with the full-length window that equals g on its support and 0 elsewhere.
+ * Lb = 0 picks the smallest admissible Lb >= max(16 Lg, 2^18) (throughput); a short Lb bounds
+ * the processing delay of block-wise / streaming use.
+ * g: Lg complex of dtype in FIR order -- entries [0, ceil(Lg/2)) are times 0, 1, ..., the rest
+ * times -floor(Lg/2), ..., -1 (host memory with DGT_G_ON_HOST, else device).  The returned plan
+ * runs dgt_execute / dgt_execute_host / dgt_plan_query / dgt_destroy; dgt_execute_inverse and
+ * dgt_window_dual return DGT_EUNSUPPORTED for it.  When Lx would not be shorter than L the
+ * function returns an ordinary full-length plan of the zero-extended window.
+ * Errors: as dgt_plan, DGT_EINVAL for Lg outside [1, L] or an Lb that is not a multiple of
+ * L_min dividing L. */
+int dgt_plan_fir(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t lambda1, int64_t lambda2,
+                 const void* g, int64_t Lg, int64_t Lb, int dtype, int flags, void* cuda_stream);
+
 /* c = DGT(f) for W signals.  f: device, W x L (complex, or real with DGT_REAL_INPUT),
  * signal-major.  c: device, W x M x N complex, n fastest (c[(w*M + m)*N + n]).  Fully
  * overwritten.  Asynchronous and stream-ordered on cuda_stream; allocates nothing.

@@ -1125,9 +1125,53 @@ __global__ void k_dual_finish(cx<T>* out, const double2* in, int64_t L, int64_t 
 }
 
 // ---------------------------------------------------------------------------------
+// shear-OLA (PAPER.md:815-831 overlap-add, 921-949 shear-OLA): the DGT with an
+// FIR window (support Lg) of a long signal as DGTs of blocks.  Block b holds f[b Lb, (b+1) Lb)
+// zero-extended to Lx >= Lb + Lg + 2a (a legal length); its length-Lx DGT with the window
+// zero-extended to Lx has, at local position p (n_local = p mod Nx), exactly the part of
+// c(m, b Lb/a + p) that comes from the block's samples -- no wrap-around reaches them, and the
+// phases agree because L_min | Lb -- so summing the blocks' coefficients over b gives c.
+// ---------------------------------------------------------------------------------
+template <typename Tin>
+__global__ void k_ola_split(Tin* x, const Tin* f, int64_t L, int64_t Lb, int64_t Lx, int64_t Nb, int64_t total) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t l = i % Lx, wb = i / Lx;
+        const int64_t w = wb / Nb, b = wb % Nb;
+        Tin v{};
+        if (l < Lb) v = f[w * L + b * Lb + l];
+        x[i] = v;
+    }
+}
+
+// c[w][m][n] = sum over blocks b with p = n - b nb (cyclic mod N) in [pmin, pmax] of
+// cb[w Nb + b][m][p mod Nx]
+template <typename T>
+__global__ void k_ola_add(cx<T>* c, const cx<T>* cb, int64_t M, int64_t N, int64_t Nx, int64_t nb, int64_t Nb,
+                          int64_t pmin, int64_t pmax, int64_t total) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = i % N, m = (i / N) % M, w = i / (N * M);
+        cx<T> acc = mk<T>(T(0), T(0));
+        // blocks whose window range covers n: b from floor((n - pmin) / nb) downwards
+        const int64_t bhi = (n - pmin) >= 0 ? (n - pmin) / nb : -((pmin - n + nb - 1) / nb);
+        const int64_t span = (pmax - pmin) / nb + 2;
+        for (int64_t db = 0; db < span && db < Nb; ++db) {
+            const int64_t b = (((bhi - db) % Nb) + Nb) % Nb;
+            int64_t p = ((n - b * nb) % N + N) % N;   // in [0, N)
+            if (p > pmax) p -= N;                      // the block's negative positions
+            if (p < pmin || p > pmax) continue;
+            const int64_t nl = ((p % Nx) + Nx) % Nx;
+            acc = acc + cb[((w * Nb + b) * M + m) * Nx + nl];
+        }
+        c[i] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // the plan
 // ---------------------------------------------------------------------------------
 
+struct Plan;
+static void free_plan(Plan* P);
 struct Plan {
     dgt_lattice_info info{};
     int dtype = DGT_C64;
@@ -1157,6 +1201,12 @@ struct Plan {
     int RB = 1, NT = 1;
     size_t smemA = 0, smemB = 0;
     int allu = 0;            // zak_kernel all-u mode (p = 1)
+    // shear-OLA (dgt_plan_fir): blocks of Lb samples zero-extended to Lx run
+    // through the inner plan; their coefficients are overlap-added
+    struct Plan* ola = nullptr;
+    int64_t ola_Lb = 0, ola_Nb = 0, ola_Ws = 0, ola_pmin = 0, ola_pmax = 0;
+    void* ola_x = nullptr;   // [Ws Nb][Lx] blocks (input type)
+    void* ola_c = nullptr;   // [Ws Nb][M][Nx] block coefficients
     int gA = 0, gB = 0;      // Zak / output kernels with per-CTA buffers in global scratch
     unsigned char* scrA = nullptr;
     unsigned char* scrB = nullptr;
@@ -1224,6 +1274,9 @@ static void prof_close(Plan* P, int h, int kind, double bytes, double flops, cud
 
 static void free_plan(Plan* P) {
     if (!P) return;
+    if (P->ola) free_plan(P->ola);
+    if (P->ola_x) cudaFree(P->ola_x);
+    if (P->ola_c) cudaFree(P->ola_c);
     void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
                     P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv, P->gt64,
                     P->scrA, P->scrB};
@@ -1686,8 +1739,43 @@ static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStrea
     return DGT_OK;
 }
 
+static int execute(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st);
+
+static int execute_ola(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) {
+    const dgt_lattice_info& I = P->info;
+    Plan* Q = P->ola;
+    const int64_t Lx = Q->info.L, Nx = Q->info.N, Nb = P->ola_Nb, nb = P->ola_Lb / I.a;
+    const bool real_in = (P->flags & DGT_REAL_INPUT) != 0;
+    const size_t ein = real_in ? P->esz / 2 : P->esz;
+    for (int64_t w0 = 0; w0 < W; w0 += P->ola_Ws) {
+        const int64_t ws = std::min<int64_t>(P->ola_Ws, W - w0);
+        const char* fw = (const char*)f + (size_t)w0 * I.L * ein;
+        const int64_t tx = ws * Nb * Lx;
+        if (P->dtype == DGT_C64) {
+            if (real_in) k_ola_split<float><<<grid_for(tx), 256, 0, st>>>((float*)P->ola_x, (const float*)fw, I.L, P->ola_Lb, Lx, Nb, tx);
+            else k_ola_split<float2><<<grid_for(tx), 256, 0, st>>>((float2*)P->ola_x, (const float2*)fw, I.L, P->ola_Lb, Lx, Nb, tx);
+        } else {
+            if (real_in) k_ola_split<double><<<grid_for(tx), 256, 0, st>>>((double*)P->ola_x, (const double*)fw, I.L, P->ola_Lb, Lx, Nb, tx);
+            else k_ola_split<double2><<<grid_for(tx), 256, 0, st>>>((double2*)P->ola_x, (const double2*)fw, I.L, P->ola_Lb, Lx, Nb, tx);
+        }
+        int rc = execute(Q, P->ola_x, P->ola_c, ws * Nb, st);
+        if (rc) return rc;
+        const int64_t tc = ws * I.M * I.N;
+        char* cw = (char*)c + (size_t)w0 * I.M * I.N * P->esz;
+        if (P->dtype == DGT_C64)
+            k_ola_add<float><<<grid_for(tc), 256, 0, st>>>((float2*)cw, (const float2*)P->ola_c, I.M, I.N, Nx, nb, Nb,
+                                                           P->ola_pmin, P->ola_pmax, tc);
+        else
+            k_ola_add<double><<<grid_for(tc), 256, 0, st>>>((double2*)cw, (const double2*)P->ola_c, I.M, I.N, Nx, nb, Nb,
+                                                            P->ola_pmin, P->ola_pmax, tc);
+        CUDA_TRY(cudaGetLastError());
+    }
+    return DGT_OK;
+}
+
 static int execute(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
+    if (P->ola) return execute_ola(P, f, c, W, st);
     const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
     if (I.branch == DGT_BRANCH_FREQ && !P->fast) {
         // front batches of P->fb signals (a multiple of the chunk), then the chunks of each
@@ -1792,6 +1880,97 @@ int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64
     return DGT_OK;
 }
 
+int dgt_plan_fir(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int64_t Lg,
+                 int64_t Lb, int dtype, int flags, void* cuda_stream) {
+    if (!out || !g) return fail(DGT_EINVAL, "null pointer");
+    *out = nullptr;
+    if (dtype != DGT_C64 && dtype != DGT_C128) return fail(DGT_EINVAL, "bad dtype");
+    if (flags & ~(DGT_REAL_INPUT | DGT_G_ON_HOST | DGT_SHEAR_PAPER | DGT_FORCE_GENERIC))
+        return fail(DGT_EINVAL, "bad flags");
+    dgt_lattice_info info{};
+    std::string err;
+    int rc = plan_lattice(L, a, M, l1, l2, flags, false, 0, 0, &info, &err);
+    if (rc) {
+        if (rc == DGT_EILLEGAL_LENGTH) g_last_lmin = info.L_min;
+        return fail(rc, err);
+    }
+    if (Lg < 1 || Lg > L) return fail(DGT_EINVAL, "window length Lg must be in [1, L]");
+    const int64_t Lmin = info.L_min;
+    const size_t esz = dtype == DGT_C64 ? 8 : 16;
+    // the window on the host, FIR layout: entries [0, ceil(Lg/2)) are times 0.., the rest
+    // times -floor(Lg/2)..-1
+    std::vector<unsigned char> gh(esz * Lg);
+    if (flags & DGT_G_ON_HOST) std::memcpy(gh.data(), g, esz * Lg);
+    else CUDA_TRY(cudaMemcpy(gh.data(), g, esz * Lg, cudaMemcpyDeviceToHost));
+    const int64_t hr = (Lg + 1) / 2, hl = Lg / 2;   // times [-hl, hr)
+    // automatic block length (throughput): the smallest multiple of L_min dividing L that is
+    // >= max(16 Lg, 2^18) -- overhead rho = (Lg + Lb)/Lb <= 1.07 and blocks long enough to fill
+    // the GPU (measured: Lb = 2^18 5.5 ms against 11.4 ms at Lb = 4 Lg, L = 2^22, Lg = 1024);
+    // else the whole signal.  Streaming callers pass a short Lb for a short delay.
+    if (Lb == 0) {
+        Lb = L;
+        const int64_t want = std::max<int64_t>(16 * Lg, (int64_t)1 << 18);
+        for (int64_t k = 1; k * Lmin <= L; ++k)
+            if (L % (k * Lmin) == 0 && k * Lmin >= want) { Lb = k * Lmin; break; }
+    }
+    if (Lb <= 0 || Lb % Lmin || L % Lb) return fail(DGT_EINVAL, "Lb must be a multiple of L_min dividing L");
+    // Lx: the smallest multiple of L_min >= Lb + Lg + 2a whose quotient by L_min is 7-smooth
+    // (the inner DFT lengths d and M' then factor into the register radices; a large prime
+    // factor would take the O(R^2) generic butterfly)
+    auto smooth = [](int64_t v) {
+        for (int64_t pr : {2, 3, 5, 7})
+            while (v % pr == 0) v /= pr;
+        return v == 1;
+    };
+    int64_t kx = (Lb + Lg + 2 * a + Lmin - 1) / Lmin;
+    while (!smooth(kx)) ++kx;
+    const int64_t Lx = kx * Lmin;
+    const bool blocks = Lx < L;
+    const int64_t Lin = blocks ? Lx : L;
+    // the window zero-extended to the inner length
+    std::vector<unsigned char> gx(esz * Lin, 0);
+    for (int64_t i = 0; i < Lg; ++i) {
+        const int64_t t = i < hr ? i : i - Lg;             // time of entry i
+        const int64_t x = ((t % Lin) + Lin) % Lin;
+        std::memcpy(gx.data() + esz * x, gh.data() + esz * i, esz);
+    }
+    dgt_plan_t inner = nullptr;
+    rc = dgt_plan(&inner, Lin, a, M, l1, l2, gx.data(), dtype, (flags & ~DGT_G_ON_HOST) | DGT_G_ON_HOST, 0, 0, 0, 0,
+                  cuda_stream);
+    if (rc) return rc;
+    if (!blocks) {   // the blocks would be as long as the signal: the full-length plan
+        *out = inner;
+        return DGT_OK;
+    }
+    Plan* P = new Plan();
+    P->info = info;
+    P->dtype = dtype;
+    P->flags = flags & ~DGT_G_ON_HOST;
+    P->esz = esz;
+    cudaGetDevice(&P->device);
+    P->ola = (Plan*)inner;
+    P->ola_Lb = Lb;
+    P->ola_Nb = L / Lb;
+    // local positions p with nonzero coefficients: a p + hr - 1 >= 0 and a p - hl <= Lb - 1
+    P->ola_pmin = -((hr - 1) / a);
+    P->ola_pmax = (Lb - 1 + hl) / a;
+    // signals per group: the block buffers stay below ~1 GiB
+    const size_t ein = (flags & DGT_REAL_INPUT) ? esz / 2 : esz;
+    const size_t per_sig = (size_t)P->ola_Nb * ((size_t)Lx * ein + (size_t)M * (Lx / a) * esz);
+    P->ola_Ws = std::max<int64_t>(1, (int64_t)((1ull << 30) / per_sig));
+    if (cudaMalloc(&P->ola_x, (size_t)P->ola_Ws * P->ola_Nb * Lx * ein) != cudaSuccess ||
+        cudaMalloc(&P->ola_c, (size_t)P->ola_Ws * P->ola_Nb * M * (Lx / a) * esz) != cudaSuccess) {
+        free_plan(P);
+        return fail(DGT_ENOMEM, "shear-OLA block buffers");
+    }
+    P->chunk = P->ola_Ws;
+    P->info.chunk = P->ola_Ws;
+    P->info.workspace_bytes = (int64_t)(P->ola_Ws * per_sig) + P->ola->info.workspace_bytes;
+    P->info.kernel_path = 16 + P->ola->info.kernel_path;   // 16 + inner path: shear-OLA
+    *out = (dgt_plan_t)P;
+    return DGT_OK;
+}
+
 int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_stream) {
     Plan* P = (Plan*)plan;
     if (!P) return fail(DGT_EINVAL, "null plan");
@@ -1809,6 +1988,7 @@ int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_s
 int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void* cuda_stream) {
     Plan* P = (Plan*)plan;
     if (!P) return fail(DGT_EINVAL, "null plan");
+    if (P->ola) return fail(DGT_EUNSUPPORTED, "synthesis is not implemented for shear-OLA plans");
     if (W < 0) return fail(DGT_EINVAL, "W < 0");
     if (W == 0) return DGT_OK;
     if (!f || !c) return fail(DGT_EINVAL, "null pointer");
@@ -1822,6 +2002,7 @@ int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void
 int dgt_window_dual(dgt_plan_t plan, int kind, void* out, int flags, void* cuda_stream) {
     Plan* P = (Plan*)plan;
     if (!P || !out) return fail(DGT_EINVAL, "null pointer");
+    if (P->ola) return fail(DGT_EUNSUPPORTED, "dual windows are not implemented for shear-OLA plans");
     if (kind != 0 && kind != 1) return fail(DGT_EINVAL, "kind must be 0 (dual) or 1 (tight)");
     if (flags & ~DGT_G_ON_HOST) return fail(DGT_EINVAL, "bad flags");
     const dgt_lattice_info& I = P->info;
@@ -2006,6 +2187,12 @@ void* dgt_debug_trace_log(dgt_plan_t plan) {
 int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W) {
     Plan* P = (Plan*)plan;
     if (!P || W <= 0) return 0;
+    if (P->ola) {   // per group of signals: split + the inner plan's launches + overlap-add
+        int64_t n = 0;
+        for (int64_t w0 = 0; w0 < W; w0 += P->ola_Ws)
+            n += 2 + dgt_launches_per_execute((dgt_plan_t)P->ola, std::min<int64_t>(P->ola_Ws, W - w0) * P->ola_Nb);
+        return n;
+    }
     const int64_t chunks = (W + P->chunk - 1) / P->chunk;
     const int64_t per = P->fast ? fast_launches_per_chunk(&P->fp) + 1 /* counter memset */ : 2;
     int64_t n = chunks * per;

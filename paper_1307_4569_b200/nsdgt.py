@@ -43,7 +43,7 @@ class KernelStat(ctypes.Structure):
                 ("bytes", ctypes.c_double), ("flops", ctypes.c_double)]
 
 
-EXPORTS = ["dgt_lattice_plan", "dgt_plan", "dgt_execute", "dgt_execute_inverse", "dgt_window_dual", "dgt_execute_host",
+EXPORTS = ["dgt_lattice_plan", "dgt_plan", "dgt_plan_fir", "dgt_execute", "dgt_execute_inverse", "dgt_window_dual", "dgt_execute_host",
            "dgt_destroy",
            "dgt_plan_query",
            "dgt_launches_per_execute", "dgt_profile_begin", "dgt_profile_end", "dgt_strerror", "dgt_last_error",
@@ -54,6 +54,8 @@ _lib.dgt_lattice_plan.argtypes = [_I64] * 5 + [_INT, _INT, _I64, _I64, ctypes.PO
 _lib.dgt_lattice_plan.restype = _INT
 _lib.dgt_plan.argtypes = [ctypes.POINTER(_P)] + [_I64] * 5 + [_P, _INT, _INT, _I64, _INT, _I64, _I64, _P]
 _lib.dgt_plan.restype = _INT
+_lib.dgt_plan_fir.argtypes = [ctypes.POINTER(_P)] + [_I64] * 5 + [_P, _I64, _I64, _INT, _INT, _P]
+_lib.dgt_plan_fir.restype = _INT
 _lib.dgt_execute.argtypes = [_P, _P, _P, _I64, _P]
 _lib.dgt_execute.restype = _INT
 _lib.dgt_execute_inverse.argtypes = [_P, _P, _P, _I64, _P]
@@ -136,7 +138,10 @@ class Plan:
     """
 
     def __init__(self, L, a, M, lam1, lam2, g, dtype="c64", real_input=False, max_chunk=0, shear=None,
-                 paper_shear=False, force_generic=False, stream=None):
+                 paper_shear=False, force_generic=False, stream=None, fir=False, Lb=0):
+        """``fir=True``: ``g`` is an FIR window of len(g) <= L taps in FIR order (entries
+        [0, ceil(Lg/2)) are times 0.., the rest negative times) and the plan is a shear-OLA plan
+        (dgt_plan_fir) with block length ``Lb`` (0 = automatic)."""
         import torch
         self.dtype = dtype
         code = _dtype_code(dtype)
@@ -156,8 +161,13 @@ class Plan:
             flags |= DGT_G_ON_HOST
         s0, s1 = shear if shear is not None else (0, 0)
         h = ctypes.c_void_p()
-        _check(_lib.dgt_plan(ctypes.byref(h), L, a, M, lam1, lam2, ctypes.c_void_p(gptr), code, flags, max_chunk,
-                             1 if shear is not None else 0, s0, s1, _stream_ptr(stream)), "dgt_plan")
+        if fir:
+            Lg = int(g_t.shape[0]) if not isinstance(g_t, np.ndarray) else int(g_t.size)
+            _check(_lib.dgt_plan_fir(ctypes.byref(h), L, a, M, lam1, lam2, ctypes.c_void_p(gptr), Lg, int(Lb), code,
+                                     flags, _stream_ptr(stream)), "dgt_plan_fir")
+        else:
+            _check(_lib.dgt_plan(ctypes.byref(h), L, a, M, lam1, lam2, ctypes.c_void_p(gptr), code, flags, max_chunk,
+                                 1 if shear is not None else 0, s0, s1, _stream_ptr(stream)), "dgt_plan")
         self._h = h
         del g_t
         info = LatticeInfo()
