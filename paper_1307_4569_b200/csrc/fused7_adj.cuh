@@ -138,14 +138,33 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
                 float2* Fc = F + (2 * h + colM) * K::FS;
                 // G' in stage-2 order: [j0/8][h][r][m2][col][oi][u]
                 const float2* g = Gq + ((((int64_t)idx * 4 + h) * NR * 16) * 2 + colM) * 64 + iM * 4 + uM;
-                dft_tile<D>(pre, tw, X2, s8, h8, 4 * colM + uM, iM, none,
+                // the G' values of a round are loaded one exchange ahead (round 0's before the
+                // first barrier, round r + 1's during round r's emit) so their latency hides
+                // behind the barrier, the exchange reads and the DFT-16
+                // (at 3 CTAs/SM only: the 5-CTA variant has no registers to spare, measured
+                // config 3 0.39 -> 0.43 ms with it; config 5 6.25 -> 6.14 ms)
+                constexpr bool GPF = MINB <= 3;
+                float2 gr[16];
+                auto load_g = [&](int r) {
+#pragma unroll
+                    for (int m2 = 0; m2 < 16; ++m2) gr[m2] = ldg_na2(g + ((int64_t)(r * 16 + m2) * 2) * 64);
+                };
+                dft_tile<D>(pre, tw, X2, s8, h8, 4 * colM + uM, iM,
+                            [&] {
+                                if (GPF) load_g(0);
+                            },
                             [&] {
                                 if (h < 3) load_r(h + 1);   // next tile's inputs behind this tile's stage 2
                             },
                             [&](int r, const float2* y) {
+                                float2 gn[16];
+                                if (!GPF) load_g(r);
+#pragma unroll
+                                for (int m2 = 0; m2 < 16; ++m2) gn[m2] = gr[m2];
+                                if (GPF && r + 1 < NR) load_g(r + 1);
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) {
-                                    float2 p = cmw(y[m2], ldg_na2(g + ((int64_t)(r * 16 + m2) * 2) * 64));
+                                    float2 p = cmw(y[m2], gn[m2]);
                                     p.x += __shfl_xor_sync(0xffffffffu, p.x, 8);
                                     p.y += __shfl_xor_sync(0xffffffffu, p.y, 8);
                                     p.x += __shfl_xor_sync(0xffffffffu, p.x, 16);
