@@ -1579,9 +1579,13 @@ static int configure(Plan* P, int64_t max_chunk) {
                                   (int)(kOutF4096Elems * e)));
     CUDA_TRY(cudaFuncSetAttribute(out_f4096_adj_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kOutF4096Elems * e)));
-    // chunk: intermediate of a chunk stays well inside L2
+    // chunk: signals per launch pair.  Up to ~1 GiB of intermediate: the launches then span
+    // many waves (config 4: 1.88 ms at 1 signal per launch, the L2-resident size; 1.49 ms at
+    // 16).  The kernels are compute- or latency-bound, so the intermediate's trip through HBM
+    // costs less than the launch tails.  NSDGT_CHUNK_L2 restores the L2-sized chunk (experiment).
     const size_t per_sig = (size_t)I.iM * I.iN * e;
     int64_t ch = std::max<int64_t>(1, (int64_t)((size_t)(l2 > 0 ? l2 : (64 << 20)) * 2 / 5 / per_sig));
+    if (!std::getenv("NSDGT_CHUNK_L2")) ch = std::max<int64_t>(ch, (int64_t)((1ull << 30) / per_sig));
     P->inv_chunk = max_chunk > 0 ? max_chunk : ch;
     if (max_chunk > 0) ch = max_chunk;
     P->chunk = ch;
