@@ -1554,6 +1554,23 @@ static int configure(Plan* P, int64_t max_chunk) {
     P->zct = (P->allu && I.d == 180 && I.q == 4 && I.c % P->RB == 0 && P->RB == (int)(64 / e) &&
               !std::getenv("NSDGT_ZAK_RT")) ? 180 : 0;
     if (P->zct) {
+        // the constant-memory twiddles of fft_ct (same values for every plan; fp64 sincospi
+        // of exact residues on the host, rounded once)
+        static std::once_flag once;
+        static int tw_rc = 0;
+        std::call_once(once, [] {
+            double2 d[180];
+            float2 f[180];
+            for (int e = 0; e < 180; ++e) {
+                const long double th = -2.0L * 3.141592653589793238462643383279502884L * (long double)e / 180.0L;
+                d[e] = make_double2((double)cosl(th), (double)sinl(th));
+                f[e] = make_float2((float)d[e].x, (float)d[e].y);
+            }
+            if (cudaMemcpyToSymbol(c_tw180d, d, sizeof(d)) != cudaSuccess ||
+                cudaMemcpyToSymbol(c_tw180f, f, sizeof(f)) != cudaSuccess)
+                tw_rc = 1;
+        });
+        if (tw_rc) return fail(DGT_ECUDA, "constant twiddle upload");
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
     }

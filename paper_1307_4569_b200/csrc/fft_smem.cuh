@@ -214,10 +214,18 @@ __device__ cx<T>* fft_smem(cx<T>* a, cx<T>* b, const Radices& rd, int nseq, int 
 // ---- compile-time variants (lengths the planner meets on hot lattices, e.g. d = 180 of
 // config 4): every index divides by a constant, composite radices run as register DFTs ----
 
+// W_180^e, e < 180, in constant memory (fft_ct's inner twiddles have warp-uniform indices:
+// constant-cache broadcasts instead of L1 data-pipe loads; filled by set_ct_twiddles)
+__constant__ double2 c_tw180d[180];
+__constant__ float2 c_tw180f[180];
+template <typename T> __device__ __forceinline__ cx<T> ctw180(int e);
+template <> __device__ __forceinline__ double2 ctw180<double>(int e) { return c_tw180d[e]; }
+template <> __device__ __forceinline__ float2 ctw180<float>(int e) { return c_tw180f[e]; }
+
 // Length-(P Q) DFT in registers, natural order in and out (Cooley-Tukey, n = Q n1 + n2,
-// k = k1 + P k2); W_{PQ}^e = tw[e * tws] from the length-N table.
+// k = k1 + P k2); W_{PQ}^e = W_N^{e tws} from the constant table (N = 180).
 template <typename T, int P, int Q>
-__device__ __forceinline__ void dft_pq(cx<T>* v, const cx<T>* __restrict__ tw, int tws) {
+__device__ __forceinline__ void dft_pq(cx<T>* v, int tws) {
     cx<T> a[P * Q];
 #pragma unroll
     for (int n2 = 0; n2 < Q; ++n2) {
@@ -226,7 +234,7 @@ __device__ __forceinline__ void dft_pq(cx<T>* v, const cx<T>* __restrict__ tw, i
         for (int n1 = 0; n1 < P; ++n1) t[n1] = v[Q * n1 + n2];
         dft_fixed<T, P>(t);
 #pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) a[n2 * P + k1] = (n2 && k1) ? cmul(t[k1], tw[n2 * k1 * tws]) : t[k1];
+        for (int k1 = 0; k1 < P; ++k1) a[n2 * P + k1] = (n2 && k1) ? cmul(t[k1], ctw180<T>(n2 * k1 * tws)) : t[k1];
     }
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) {
@@ -253,10 +261,18 @@ __device__ __forceinline__ void stage_ct(const cx<T>* __restrict__ in, cx<T>* __
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = src[j + r * nb];
         if (NS > 1) {
+            // W^{r k tstep} = (W^{k tstep})^r: one table load per butterfly (the lane-varying
+            // index would cost a scattered load per element), powers by multiplication
+            const cx<T> w1 = tw[k * tstep];
+            cx<T> wr = w1;
+            v[1] = cmul(v[1], w1);
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r * k * tstep]);
+            for (int r = 2; r < R; ++r) {
+                wr = cmul(wr, w1);
+                v[r] = cmul(v[r], wr);
+            }
         }
-        if constexpr (Q > 1) dft_pq<T, P, Q>(v, tw, N / R);
+        if constexpr (Q > 1) dft_pq<T, P, Q>(v, N / R);
         else dft_fixed<T, P>(v);
         const int base = (j / NS) * NS * R + k;
 #pragma unroll
