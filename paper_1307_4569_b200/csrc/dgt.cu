@@ -621,13 +621,13 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
 //   pass 1 (lane t):         Y(t, k1)  = W_4096^{t k1} sum_r x(t + 256 r) W_16^{r k1}
 //   pass 2 (lane k1, t1):    Z(k1, t1, k2) = W_256^{t1 k2} sum_t2 Y(t1 + 16 t2, k1) W_16^{t2 k2}
 //   pass 3 (lane k1, k2):    X(k1 + 16 k2 + 256 k3) = sum_t1 Z(k1, t1, k2) W_16^{t1 k3}
-// v[k] *= W_4096^{s k}, k = 1..15, from four table loads (W^s, W^2s, W^4s, W^8s) and eleven
-// products (at most three roundings per twiddle; fifteen scattered loads per lane was the
+// v[k] *= W_4096^{s k}, k = 1..15, from one table load (W^s), three squarings and eleven
+// products (at most six roundings per twiddle; fifteen scattered loads per lane was the
 // kernel's largest L1 cost)
 template <typename C>
 __device__ __forceinline__ void twiddle15(C* v, const C* __restrict__ tw, int s) {
-    const C w1 = __ldg(tw + (s & 4095)), w2 = __ldg(tw + ((2 * s) & 4095));
-    const C w4 = __ldg(tw + ((4 * s) & 4095)), w8 = __ldg(tw + ((8 * s) & 4095));
+    const C w1 = __ldg(tw + (s & 4095));
+    const C w2 = cmul(w1, w1), w4 = cmul(w2, w2), w8 = cmul(w4, w4);   // squarings: one load
     const C w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
     v[1] = cmul(v[1], w1); v[2] = cmul(v[2], w2); v[3] = cmul(v[3], w3); v[4] = cmul(v[4], w4);
     v[5] = cmul(v[5], w5); v[6] = cmul(v[6], w6); v[7] = cmul(v[7], w7); v[8] = cmul(v[8], w8);
