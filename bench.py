@@ -195,14 +195,15 @@ def run_reference(args, wl, ws, rank):
     per_step = max(1.0, min(6.0, 150.0 / max(1, args.steps + args.warmup)))
     times, vals = [], []
     desc, cores = "", 0
+    sample = oracle_sample_inverse if args.inverse else oracle_sample
     for i in range(args.warmup + args.steps):
-        v, cores, desc, dt = oracle_sample(wl, per_step)
+        v, cores, desc, dt = sample(wl, per_step)
         if i >= args.warmup:
             times.append(dt)
             vals.append(v)
     value = statistics.median(vals)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC_INV if args.inverse else METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, synthetic/workloads.py)",
