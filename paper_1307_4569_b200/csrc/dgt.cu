@@ -1725,8 +1725,13 @@ static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStrea
     if (P->fast && !P->inv_generic) {
         // fused synthesis (fused7_adj.cuh) on the forward ring
         const int ph = prof_open(P, st);
-        int rc = launch_fast_adj(&P->fp, c, P->Cws, f, W, st);
-        if (rc) return rc;
+        const int64_t chunk = fast_chunk(&P->fp);
+        for (int64_t w0 = 0; w0 < W; w0 += chunk) {
+            const int64_t wc = std::min<int64_t>(chunk, W - w0);
+            int rc = launch_fast_adj(&P->fp, (const char*)c + (size_t)w0 * I.M * I.N * 8,
+                                     P->Cws, (char*)f + (size_t)w0 * I.L * 8, wc, st);
+            if (rc) return rc;
+        }
         const double L = (double)I.L, MN = (double)I.M * (double)I.N;
         prof_close(P, ph, PK_FASTADJ, W * (L + MN) * 8.0 + L * 8.0,
                    W * (8.0 * L * I.q + 4.0 * L * std::log2((double)I.d) + 4.0 * MN * std::log2((double)I.d) +

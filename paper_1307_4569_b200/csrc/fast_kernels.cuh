@@ -200,7 +200,8 @@ inline size_t fast_workspace_bytes(const FastPlan* fp, int64_t /*Wc*/) {
 }
 
 // the fused kernel consumes the whole batch in one launch
-inline int64_t fast_chunk(const FastPlan*) { return (int64_t)1 << 40; }
+// (the kernel's 32-bit job indices bound one launch to W (nA + nB) < 2^31 signals' jobs)
+inline int64_t fast_chunk(const FastPlan* fp) { return (((int64_t)1 << 31) - 1) / (fp->nA + fp->nB); }
 inline int64_t fast_launches_per_chunk(const FastPlan*) { return 1; }
 
 template <typename T>
