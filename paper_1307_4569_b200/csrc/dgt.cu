@@ -367,7 +367,8 @@ __global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
         }
     }
     __syncthreads();
-    C* phi = fft_ct<T, D>(R1, R2, RBC, tw);     // Phi in R1[0, RBC D)
+    C* phi = fft_ct<T, D>(R1, R2, RBC, tw);     // Phi in the first RBC D of R1 or R2
+    C* Yb = phi == R1 ? R2 : R1;
     {
         const C* __restrict__ G = (const C*)A.G;
         C gv[NP];
@@ -382,11 +383,11 @@ __global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
 #pragma unroll
         for (int it = 0; it < NP; ++it) {
             const int i = tid + it * NT;
-            if (i < Q * RBC * D) R2[i] = cmul(phi[i % (RBC * D)], gv[it]);
+            if (i < Q * RBC * D) Yb[i] = cmul(phi[i % (RBC * D)], gv[it]);
         }
     }
     __syncthreads();
-    C* Y = fft_ct<T, D>(R2, R1, Q * RBC, tw);    // result in R2
+    C* Y = fft_ct<T, D>(Yb, phi, Q * RBC, tw);   // Phi is dead: its buffer is the scratch
     C* Cw = (C*)A.C + w * A.iM * Q * D;
     const int jbase = r0 + c * (l % Q);
 #pragma unroll
@@ -881,7 +882,8 @@ __global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fou
         }
     }
     __syncthreads();
-    C* Y = fft_ct<T, D>(R1, R2, Q * RBC, tw);   // in R1
+    C* Y = fft_ct<T, D>(R1, R2, Q * RBC, tw);   // in R1 or R2
+    C* Acc = Y == R1 ? R2 : R1;
     {
         const C* __restrict__ G = (const C*)A.G;
 #pragma unroll
@@ -893,12 +895,12 @@ __global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fou
 #pragma unroll
                 for (int u = 1; u < Q; ++u)
                     acc = acc + cmul(Y[(u * RBC + rr) * D + nu], __ldg(G + ((r0 + rr) * Q + u) * D + nu));
-                R2[i] = acc;
+                Acc[i] = acc;
             }
         }
     }
     __syncthreads();
-    C* R = fft_ct<T, D>(R2, R1 + Q * RBC * D - RBC * D, RBC, tw);   // scratch: the tail of R1 (Y is dead)
+    C* R = fft_ct<T, D>(Acc, Y, RBC, tw);   // Y is dead: its buffer is the scratch
     const C* __restrict__ chirp = (const C*)A.chirp;
     C* fo = (C*)fout + w * A.L;
 #pragma unroll
@@ -1242,7 +1244,7 @@ struct Plan {
 enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_ZAKADJ = 6,
                 PK_OUTADJ = 7, PK_FASTADJ = 8, PK_COUNT = 9 };
 static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
-                                           "zak_ct_d180", "out_f4096", "zak_adjoint", "out_adjoint",
+                                           "zak_ct", "out_f4096", "zak_adjoint", "out_adjoint",
                                            "fused7a_t_p1"};
 
 static cudaEvent_t prof_event(Plan* P) {
@@ -1468,6 +1470,8 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
         zak_ct_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     else if (P->zct == 180)
         zak_ct_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+    else if (P->zct == 720)
+        zak_ct_kernel<T, 720, 4, 1><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     else
         zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->gA ? 0 : P->smemA, st>>>(A);
     prof_close(P, ph, P->zct ? PK_ZAKCT : PK_ZAK, by_in, fl_zak, st);
@@ -1550,29 +1554,36 @@ static int configure(Plan* P, int64_t max_chunk) {
     P->NT = nt;
     P->smemB = smemB(nt);
     CUDA_TRY(cudaFuncSetAttribute(zak_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gA ? 0 : (int)P->smemA));
-    // compile-time Zak kernel: d = 180, q = 4, p = 1, RB = 64 / e columns dividing c
-    P->zct = (P->allu && I.d == 180 && I.q == 4 && I.c % P->RB == 0 && P->RB == (int)(64 / e) &&
-              !std::getenv("NSDGT_ZAK_RT")) ? 180 : 0;
+    // compile-time Zak kernels (p = 1, q = 4, all-u mode): d = 180 with RB = 64 / e columns
+    // (config 4), d = 720 with one column per CTA (config 2)
+    P->zct = 0;
+    if (P->allu && I.q == 4 && I.c % P->RB == 0 && !std::getenv("NSDGT_ZAK_RT")) {
+        if (I.d == 180 && P->RB == (int)(64 / e)) P->zct = 180;
+        if (I.d == 720 && P->RB == 1) P->zct = 720;
+    }
     if (P->zct) {
-        // the constant-memory twiddles of fft_ct (same values for every plan; fp64 sincospi
-        // of exact residues on the host, rounded once)
+        // the constant-memory twiddles of fft_ct (same values for every plan; long-double
+        // cos/sin of exact residues on the host, rounded once)
         static std::once_flag once;
         static int tw_rc = 0;
         std::call_once(once, [] {
-            double2 d[180];
-            float2 f[180];
-            for (int e = 0; e < 180; ++e) {
-                const long double th = -2.0L * 3.141592653589793238462643383279502884L * (long double)e / 180.0L;
-                d[e] = make_double2((double)cosl(th), (double)sinl(th));
-                f[e] = make_float2((float)d[e].x, (float)d[e].y);
-            }
-            if (cudaMemcpyToSymbol(c_tw180d, d, sizeof(d)) != cudaSuccess ||
-                cudaMemcpyToSymbol(c_tw180f, f, sizeof(f)) != cudaSuccess)
-                tw_rc = 1;
+            auto fill = [](auto& dsym, auto& fsym, int n) {
+                std::vector<double2> d(n);
+                std::vector<float2> f(n);
+                for (int k = 0; k < n; ++k) {
+                    const long double th = -2.0L * 3.141592653589793238462643383279502884L * (long double)k / (long double)n;
+                    d[k] = make_double2((double)cosl(th), (double)sinl(th));
+                    f[k] = make_float2((float)d[k].x, (float)d[k].y);
+                }
+                return cudaMemcpyToSymbol(dsym, d.data(), sizeof(double2) * n) == cudaSuccess &&
+                       cudaMemcpyToSymbol(fsym, f.data(), sizeof(float2) * n) == cudaSuccess;
+            };
+            if (!fill(c_tw180d, c_tw180f, 180) || !fill(c_tw720d, c_tw720f, 720)) tw_rc = 1;
         });
         if (tw_rc) return fail(DGT_ECUDA, "constant twiddle upload");
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+        CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 720, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
     }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     // out_f4096: 2 CTAs per SM for c128 (128 registers, measured faster than 3 CTAs at 80
@@ -1591,6 +1602,7 @@ static int configure(Plan* P, int64_t max_chunk) {
     if (P->zct) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+        CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 720, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
     }
     CUDA_TRY(cudaFuncSetAttribute(out_f4096_adj_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kOutF4096Elems * e)));
@@ -1695,6 +1707,8 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
         zak_ct_adj_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
     else if (P->zct == 180)
         zak_ct_adj_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
+    else if (P->zct == 720)
+        zak_ct_adj_kernel<T, 720, 4, 1><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
     else
         zak_adj_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->gA ? 0 : P->smemAinv, st>>>(A, zout);
     prof_close(P, ph, PK_ZAKADJ, Wc * L * e + L * e, Wc * (8.0 * L * I.q / I.p + 4.0 * L * lg_d + 4.0 * MN * lg_d), st);

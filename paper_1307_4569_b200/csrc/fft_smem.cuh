@@ -218,13 +218,22 @@ __device__ cx<T>* fft_smem(cx<T>* a, cx<T>* b, const Radices& rd, int nseq, int 
 // constant-cache broadcasts instead of L1 data-pipe loads; filled by set_ct_twiddles)
 __constant__ double2 c_tw180d[180];
 __constant__ float2 c_tw180f[180];
-template <typename T> __device__ __forceinline__ cx<T> ctw180(int e);
-template <> __device__ __forceinline__ double2 ctw180<double>(int e) { return c_tw180d[e]; }
-template <> __device__ __forceinline__ float2 ctw180<float>(int e) { return c_tw180f[e]; }
+__constant__ double2 c_tw720d[720];
+__constant__ float2 c_tw720f[720];
+template <typename T, int N> __device__ __forceinline__ cx<T> ctw(int e) {
+    static_assert(N == 180 || N == 720, "constant twiddle tables exist for N = 180, 720");
+    if constexpr (N == 180) {
+        if constexpr (sizeof(cx<T>) == 16) return c_tw180d[e];
+        else return c_tw180f[e];
+    } else {
+        if constexpr (sizeof(cx<T>) == 16) return c_tw720d[e];
+        else return c_tw720f[e];
+    }
+}
 
 // Length-(P Q) DFT in registers, natural order in and out (Cooley-Tukey, n = Q n1 + n2,
 // k = k1 + P k2); W_{PQ}^e = W_N^{e tws} from the constant table (N = 180).
-template <typename T, int P, int Q>
+template <typename T, int P, int Q, int N>
 __device__ __forceinline__ void dft_pq(cx<T>* v, int tws) {
     cx<T> a[P * Q];
 #pragma unroll
@@ -234,7 +243,7 @@ __device__ __forceinline__ void dft_pq(cx<T>* v, int tws) {
         for (int n1 = 0; n1 < P; ++n1) t[n1] = v[Q * n1 + n2];
         dft_fixed<T, P>(t);
 #pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) a[n2 * P + k1] = (n2 && k1) ? cmul(t[k1], ctw180<T>(n2 * k1 * tws)) : t[k1];
+        for (int k1 = 0; k1 < P; ++k1) a[n2 * P + k1] = (n2 && k1) ? cmul(t[k1], ctw<T, N>(n2 * k1 * tws)) : t[k1];
     }
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) {
@@ -272,7 +281,7 @@ __device__ __forceinline__ void stage_ct(const cx<T>* __restrict__ in, cx<T>* __
                 v[r] = cmul(v[r], wr);
             }
         }
-        if constexpr (Q > 1) dft_pq<T, P, Q>(v, N / R);
+        if constexpr (Q > 1) dft_pq<T, P, Q, N>(v, N / R);
         else dft_fixed<T, P>(v);
         const int base = (j / NS) * NS * R + k;
 #pragma unroll
@@ -280,17 +289,29 @@ __device__ __forceinline__ void stage_ct(const cx<T>* __restrict__ in, cx<T>* __
     }
 }
 
-// DFT of nseq sequences of compile-time length N (stride N); returns the result buffer.
-// N = 180: radix 15 (3 x 5) then 12 (4 x 3) -- odd first-pass write stride, so the
-// 16-byte stores of a quarter warp hit distinct banks.
+// DFT of nseq sequences of compile-time length N (stride N); returns the result buffer (a or
+// b -- callers use the returned pointer).  The first pass has an odd radix, so its write stride
+// is odd and the 16-byte stores of a quarter warp hit distinct banks.
+//   N = 180 (config 4): radix 15 (3 x 5), then 12 (4 x 3)          -> result in a
+//   N = 720 (config 2): radix 9 (3 x 3), then 16, then 5            -> result in b
 template <typename T, int N>
 __device__ cx<T>* fft_ct(cx<T>* a, cx<T>* b, int nseq, const cx<T>* __restrict__ tw) {
-    static_assert(N == 180, "fft_ct: add a radix plan for this length");
-    stage_ct<T, 180, 3, 5, 1>(a, b, nseq, tw);
-    __syncthreads();
-    stage_ct<T, 180, 4, 3, 15>(b, a, nseq, tw);
-    __syncthreads();
-    return a;
+    static_assert(N == 180 || N == 720, "fft_ct: add a radix plan for this length");
+    if constexpr (N == 180) {
+        stage_ct<T, 180, 3, 5, 1>(a, b, nseq, tw);
+        __syncthreads();
+        stage_ct<T, 180, 4, 3, 15>(b, a, nseq, tw);
+        __syncthreads();
+        return a;
+    } else {
+        stage_ct<T, 720, 3, 3, 1>(a, b, nseq, tw);
+        __syncthreads();
+        stage_ct<T, 720, 16, 1, 9>(b, a, nseq, tw);
+        __syncthreads();
+        stage_ct<T, 720, 5, 1, 144>(a, b, nseq, tw);
+        __syncthreads();
+        return b;
+    }
 }
 
 // Host: split n into radices (16, 8, 4, 2 for powers of two; then 5, 3; then primes).

@@ -311,3 +311,26 @@ def test_large_inner_length_global_scratch(torch_cuda, nsdgt, oracle_mod, lam2):
     cr = np.random.default_rng(5).standard_normal((M, L // a)) + 0j
     fi = plan.inverse(torch.from_numpy(cr).cuda()).cpu().numpy()
     assert rel(fi, oracle_mod.idgt(cr, g, a, M, lam1, lam2)) <= TOL["c128"]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_config2_compile_time_zak_matches_runtime(torch_cuda, nsdgt, oracle_mod, dtype, monkeypatch):
+    """Config 2's lattice (d = 720): the compile-time Zak kernels (radix 9, 16, 5) against the
+    runtime-radix kernels, forward and synthesis, and against the oracle on sampled columns."""
+    torch = torch_cuda
+    wl = CONFIGS[1]
+    g = window(wl)
+    f = batch(wl, 0, 2).astype(np.complex64 if dtype == "c64" else np.complex128)
+    ft = torch.from_numpy(f).cuda()
+    pc = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
+    cc = pc.execute(ft)
+    fc = pc.inverse(cc)
+    monkeypatch.setenv("NSDGT_ZAK_RT", "1")
+    pr = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
+    cr = pr.execute(ft)
+    fr = pr.inverse(cr)
+    assert rel(cc.cpu().numpy(), cr.cpu().numpy()) <= TOL[dtype]
+    assert rel(fc.cpu().numpy(), fr.cpu().numpy()) <= TOL[dtype]
+    cols = np.sort(np.random.default_rng(2).choice(wl.N, 16, replace=False))
+    ref = oracle_mod.dgt(f, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols)
+    assert rel(cc[:, :, torch.from_numpy(cols).cuda()].cpu().numpy(), ref) <= TOL[dtype]
