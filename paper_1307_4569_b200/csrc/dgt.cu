@@ -536,11 +536,12 @@ __device__ __forceinline__ void fb_column(const OutArgs& A, C* out, unsigned lon
     }
 }
 
-template <typename T>
+// IMCT > 0: compile-time inner channel count (its DFT by fft_ct; config 2: 200)
+template <typename T, int IMCT = 0>
 __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
-    const int64_t iM = A.iM, iN = A.iN, q = A.q, d = A.d;
+    const int64_t iM = IMCT ? IMCT : A.iM, iN = A.iN, q = A.q, d = A.d;
     const int NT = A.NT;
     const int iMi = (int)iM, qi = (int)q, di = (int)d;
     // column cl of this CTA is inner n = nb + ns * cl: T-branch nb = x NT, ns = 1 (consecutive
@@ -589,7 +590,9 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
         }
     }
     __syncthreads();
-    C* X = fft_smem<T>(bufA, bufB, A.rd, nt, (int)iM, (const C*)A.tw);
+    C* X;
+    if constexpr (IMCT > 0) X = fft_ct<T, IMCT>(bufA, bufB, nt, (const C*)A.tw);
+    else X = fft_smem<T>(bufA, bufB, A.rd, nt, (int)iM, (const C*)A.tw);
     if (A.branch != DGT_BRANCH_FREQ) {
         // c[w][(m - rot(n)) mod M][n] = E(n) * X(m, n)   (Alg. 1 lines 9-12)
         C* out = (C*)A.out + w * A.M * A.N;
@@ -1220,6 +1223,7 @@ struct Plan {
     void* finv = nullptr;
     int zct = 0;             // zak_kernel compile-time inner length (0 = runtime radices)
     int inv_generic = 0;     // experiment knob (NSDGT_INV_GENERIC, read at plan time): generic synthesis
+    int outct = 0;           // out_kernel compile-time inner channel count (0 = runtime radices)
     int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
     int fast = 0;  // specialised path id (0 = generic)
     FastPlan fp{};
@@ -1501,6 +1505,8 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
         out_f4096_kernel<T, 3><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
     else if (P->outk == 2)
         out_f4096_kernel<T, 2><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+    else if (P->outct == 200)
+        out_kernel<T, 200><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
     else
         out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->gB ? 0 : P->smemB, st>>>(B);
     prof_close(P, ph, P->outk ? PK_OUTF : PK_OUT, by_out, fl_out, st);
@@ -1586,6 +1592,9 @@ static int configure(Plan* P, int64_t max_chunk) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 720, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
     }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
+    // compile-time output DFT for M' = 200 (config 2, time shear)
+    P->outct = (I.branch != DGT_BRANCH_FREQ && I.iM == 200 && !P->gB && !std::getenv("NSDGT_OUT_GENERIC")) ? 200 : 0;
+    if (P->outct) CUDA_TRY(cudaFuncSetAttribute(out_kernel<T, 200>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
     // out_f4096: 2 CTAs per SM for c128 (128 registers, measured faster than 3 CTAs at 80
     // registers with spills), 3 for c64
     P->outk = (I.branch == DGT_BRANCH_FREQ && I.iM == 4096 && !std::getenv("NSDGT_OUT_GENERIC")) ? (e == 16 ? 2 : 1) : 0;

@@ -294,10 +294,20 @@ __device__ __forceinline__ void stage_ct(const cx<T>* __restrict__ in, cx<T>* __
 // is odd and the 16-byte stores of a quarter warp hit distinct banks.
 //   N = 180 (config 4): radix 15 (3 x 5), then 12 (4 x 3)          -> result in a
 //   N = 720 (config 2): radix 9 (3 x 3), then 16, then 5            -> result in b
+//   N = 200 (config 2's output DFT): radix 5, then 8, then 5         -> result in b
 template <typename T, int N>
 __device__ cx<T>* fft_ct(cx<T>* a, cx<T>* b, int nseq, const cx<T>* __restrict__ tw) {
-    static_assert(N == 180 || N == 720, "fft_ct: add a radix plan for this length");
-    if constexpr (N == 180) {
+    static_assert(N == 180 || N == 720 || N == 200, "fft_ct: add a radix plan for this length");
+    if constexpr (N == 200) {
+        stage_ct<T, 200, 5, 1, 1>(a, b, nseq, tw);
+        __syncthreads();
+        stage_ct<T, 200, 8, 1, 5>(b, a, nseq, tw);
+        __syncthreads();
+        stage_ct<T, 200, 5, 1, 40>(a, b, nseq, tw);
+        __syncthreads();
+        return b;
+    }
+    else if constexpr (N == 180) {
         stage_ct<T, 180, 3, 5, 1>(a, b, nseq, tw);
         __syncthreads();
         stage_ct<T, 180, 4, 3, 15>(b, a, nseq, tw);

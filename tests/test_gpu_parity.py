@@ -315,8 +315,9 @@ def test_large_inner_length_global_scratch(torch_cuda, nsdgt, oracle_mod, lam2):
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_config2_compile_time_zak_matches_runtime(torch_cuda, nsdgt, oracle_mod, dtype, monkeypatch):
-    """Config 2's lattice (d = 720): the compile-time Zak kernels (radix 9, 16, 5) against the
-    runtime-radix kernels, forward and synthesis, and against the oracle on sampled columns."""
+    """Config 2's lattice (d = 720, M' = 200): the compile-time Zak kernels (radix 9, 16, 5) and
+    output DFT (radix 5, 8, 5) against the runtime-radix kernels, forward and synthesis, and
+    against the oracle on sampled columns."""
     torch = torch_cuda
     wl = CONFIGS[1]
     g = window(wl)
@@ -326,6 +327,7 @@ def test_config2_compile_time_zak_matches_runtime(torch_cuda, nsdgt, oracle_mod,
     cc = pc.execute(ft)
     fc = pc.inverse(cc)
     monkeypatch.setenv("NSDGT_ZAK_RT", "1")
+    monkeypatch.setenv("NSDGT_OUT_GENERIC", "1")
     pr = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
     cr = pr.execute(ft)
     fr = pr.inverse(cr)
