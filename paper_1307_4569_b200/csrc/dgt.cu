@@ -1400,9 +1400,7 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
         k_phase_table<T><<<grid_for(2 * I.N), 256, 0, st>>>((C*)P->ptab, I.N);
     }
     CUDA_TRY(cudaGetLastError());
-    // the fused kernels load complex input: real-input plans take the generic kernels (they
-    // promote real samples on load)
-    int rc = build_fast<T>(&P->fp, P->info, gt, P->E, (P->flags & (DGT_FORCE_GENERIC | DGT_REAL_INPUT)) != 0, st);
+    int rc = build_fast<T>(&P->fp, P->info, gt, P->E, (P->flags & DGT_FORCE_GENERIC) != 0, st);
     if (rc) return rc;
     P->fast = P->fp.kind;
     CUDA_TRY(cudaStreamSynchronize(st));

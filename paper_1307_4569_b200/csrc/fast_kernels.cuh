@@ -41,6 +41,7 @@ struct FastPlan {
     void* Gpa = nullptr;         // G' in the adjoint kernel's order (owned)
     size_t smem_adj = 0;
     int grid_adj = 0, lag_adj = 0;   // synthesis kernel grid and look-ahead
+    int grid_real = 0;               // real-input forward kernel grid
     int dbg = 0;                 // experiment knobs (NSDGT_DBG, read once at plan time; fused7.cuh)
     unsigned long long* tracelog = nullptr;   // dbg & 16: per-CTA phase stamps of a -DNSDGT_TRACE build
     int* counters = nullptr;     // job queue + per-slot completion counters (owned)
@@ -49,6 +50,11 @@ struct FastPlan {
 template <int D, int MINB>
 static void launch7(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
     v7::fused7_kernel<D, MINB><<<grid, v7::Cfg<D>::NT, smem, st>>>(a);
+}
+// real input (promoted on load): the default CTAs-per-SM variants only
+template <int D, int MINB>
+static void launch7r(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
+    v7::fused7_kernel<D, MINB, (MINB <= 3), true><<<grid, v7::Cfg<D>::NT, smem, st>>>(a);
 }
 template <int D, int MINB>
 static void launch7a(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
@@ -172,6 +178,16 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
             return DGT_ECUDA;
         fp->grid_adj = std::min(per_sm * sms, per_sm_a * sms);
     }
+    {   // real-input variant (default occupancy): attribute + resident grid
+        const void* kr = D == 512 ? (const void*)v7::fused7_kernel<512, 3, true, true>
+                                  : (const void*)v7::fused7_kernel<256, 5, false, true>;
+        int per_sm_r = 0;
+        if (cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_r, kr, v7::Cfg<512>::NT, smem) != cudaSuccess ||
+            per_sm_r < 1)
+            return DGT_ECUDA;
+        fp->grid_real = std::min(per_sm * sms, per_sm_r * sms);
+    }
     fp->dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;   // experiment knobs
     if (fp->dbg & 16) {   // phase trace of a -DNSDGT_TRACE build (tools/v7trace.py, dgt_debug_trace_log)
         if (cudaMalloc(&fp->tracelog, sizeof(unsigned long long) * 8 * 4096) != cudaSuccess) return DGT_ENOMEM;
@@ -206,7 +222,7 @@ inline int64_t fast_launches_per_chunk(const FastPlan*) { return 1; }
 
 template <typename T>
 int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int64_t W, cudaStream_t st) {
-    if (real_in || fp->kind != 2) return DGT_EUNSUPPORTED;
+    if (fp->kind != 2) return DGT_EUNSUPPORTED;
     if (W * (int64_t)(fp->nA + fp->nB) >= (int64_t)1 << 31) return DGT_EUNSUPPORTED;   // 32-bit job indices
     const int nctr = 1 + 2 * fp->S;
     if (!fp->counters) return DGT_EINVAL;   // allocated by build_fast
@@ -220,8 +236,14 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
         cudaMemsetAsync(fp->tracelog, 0, sizeof(unsigned long long) * 8 * 4096, st);
         a.log = fp->tracelog;
     }
-    if (fp->D == 512) (fp->minb == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st);
-    else (fp->minb == 5 ? launch7<256, 5> : fp->minb == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st);
+    if (real_in) {   // the real variants are compiled for the default occupancy only
+        if (fp->D == 512) launch7r<512, 3>(a, fp->grid_real, fp->smem, st);
+        else launch7r<256, 5>(a, fp->grid_real, fp->smem, st);
+    } else if (fp->D == 512) {
+        (fp->minb == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st);
+    } else {
+        (fp->minb == 5 ? launch7<256, 5> : fp->minb == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st);
+    }
     return DGT_OK;
 }
 

@@ -308,7 +308,7 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
 
 // FULLPF: the whole next tile's inputs are prefetched behind the current tile's stage 2
 // (fits the 168-register budget of 3 CTAs/SM; with 4+ CTAs only the first half).
-template <int D, int MINB, bool FULLPF = (MINB <= 3)>
+template <int D, int MINB, bool FULLPF = (MINB <= 3), bool REAL = false>
 __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     using K = Cfg<D>;
     constexpr int R1 = K::R1, Q = K::Q, M = D, AC = K::ACOL, BT = K::BT;
@@ -350,9 +350,15 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     // cross-tile prefetch within the register budget) ----
     float2 pre[R1];
     auto load_f = [&](int w, int j0, int b) {   // Zak DFT input: column j0 + s8, rows t + 16 k
-        const float2* fw = A.f + (int64_t)w * M * D + j0 + s8;
+        if constexpr (REAL) {   // real samples (4-byte loads, 32 contiguous bytes per row of 8 columns)
+            const float* fr = reinterpret_cast<const float*>(A.f) + (int64_t)w * M * D + j0 + s8;
 #pragma unroll
-        for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ldg_na2(fw + (int64_t)(h8 + 16 * k) * M);
+            for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = make_float2(__ldcs(fr + (int64_t)(h8 + 16 * k) * M), 0.f);
+        } else {
+            const float2* fw = A.f + (int64_t)w * M * D + j0 + s8;
+#pragma unroll
+            for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ldg_na2(fw + (int64_t)(h8 + 16 * k) * M);
+        }
     };
     // G' of product tile h (slot s8 = 4 col + u, lane t).  Layout [j0 / 8][h][kp][t][slot] of
     // float4 (k = 2 kp, 2 kp + 1): a warp reads 512 contiguous bytes.

@@ -130,14 +130,14 @@ def test_repeat_execute_deterministic(env):
 
 
 def test_real_input_on_fused_lattice(env):
-    """A real-input plan on config 3's lattice (the fused kernels load complex input, so the plan
-    takes the generic kernels) matches the oracle and the complex-input fused plan."""
+    """A real-input plan on config 3's lattice (fused7 promotes real samples on load) matches the
+    oracle and the complex-input fused plan."""
     torch, nsdgt, oracle = env
     wl = CONFIGS[2]
     g = window(wl)
     f = np.random.default_rng(11).standard_normal((2, wl.L)).astype(np.float32)
     pr = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c64", real_input=True)
-    assert pr.info["kernel_path"] == 0
+    assert pr.info["kernel_path"] == 2
     cr = pr.execute(torch.from_numpy(f).cuda()).cpu().numpy()
     pc = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c64")
     cc = pc.execute(torch.from_numpy(f.astype(np.complex64)).cuda()).cpu().numpy()
