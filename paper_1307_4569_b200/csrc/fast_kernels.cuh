@@ -145,15 +145,15 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     fp->beta = (int)beta;
     // Look-ahead: B(w) is queued lag signals after A(w).  An A job spans several tiles, so about
     // 3 x (CTAs / jobs per signal) signals of look-ahead hide the A -> B dependency; the ring
-    // (S signals of intermediate) is capped at ~80 MB so that it stays mostly in L2, with at
-    // least 4 slots beyond the look-ahead (config 5: S = 10, lag = 6, 5.78 ms; the earlier
-    // 64 MB cap gave S = 8, lag = 5, 5.91 ms).
+    // (S signals of intermediate) is capped at ~80 MB so that it stays mostly in L2, with
+    // 4 + lag/2 slots beyond the look-ahead where it fits (config 5: S = 10, lag = 6, 5.78 ms;
+    // the earlier 64 MB cap gave S = 8, lag = 5, 5.91 ms).
     {
         const int jps = fp->nA + fp->nB;
         const size_t per_sig = (size_t)M * Q * D * sizeof(float2);
         const int smax = std::max(6, (int)((80ull << 20) / per_sig));
         fp->lag = std::max(2, std::min(smax - 4, (3 * fp->grid + jps / 2) / jps));
-        fp->S = std::min(smax, fp->lag + 3 + fp->lag / 4);
+        fp->S = std::min(smax, fp->lag + 4 + fp->lag / 2);   // config 3: S = 38 (0.341 ms; 31: 0.354)
     }
     if (const char* e = std::getenv("NSDGT_S")) fp->S = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("NSDGT_LAG")) fp->lag = std::max(0, std::atoi(e));
