@@ -80,6 +80,14 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
         if (!decode(jobsm, A.W, A.lag, A.nB, A.nA, &isB, &w, &idx)) break;
         const int gen = w / A.S, slot = w - gen * A.S;
         float2* wsl = A.ws + (int64_t)slot * MN;
+        // B' reads only the (read-only) coefficients; its dependency gates the ring stores, so
+        // its first tile's loads are issued before the wait and overlap it
+        auto load_c = [&](int bt) {
+            const float2* src = A.f + (int64_t)w * MN + idx * 16 + 8 * bt + s8;
+#pragma unroll
+            for (int k = 0; k < R1; ++k) pre[k] = ldg_na2(src + (int64_t)(h8 + 16 * k) * N);
+        };
+        if (isB) load_c(0);
         if (tid == 0 && !(A.dbg & 1)) {
             // B': slot free (all A'(w - S) done); A': all B'(w) done
             if (isB) spin_until(doneA + slot, gen * A.nA);
@@ -88,17 +96,12 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
         __syncthreads();   // every thread's ring accesses follow thread 0's acquire
         if (isB) {
             // ---------------- pass B': columns n = 16 idx .. 16 idx + 15 ----------------
-            // tile bt's input: column n = 16 idx + 8 bt + s8, rows m = t + 16 k (conjugated when used)
-            auto load_c = [&](int bt) {
-                const float2* src = A.f + (int64_t)w * MN + idx * 16 + 8 * bt + s8;
-#pragma unroll
-                for (int k = 0; k < R1; ++k) pre[k] = ldg_na2(src + (int64_t)(h8 + 16 * k) * N);
-            };
+            // tile bt's input: column n = 16 idx + 8 bt + s8, rows m = t + 16 k (conjugated when
+            // used); tile 0's was issued before the dependency wait
 #pragma unroll 1
             for (int bt = 0; bt < 2; ++bt) {
                 const int n = idx * 16 + 8 * bt + s8;
                 const float2 e = ldg_na2(A.E + n);
-                if (bt == 0) load_c(0);
 #pragma unroll
                 for (int k = 0; k < R1; ++k) pre[k] = conjf2(pre[k]);
                 if (bt) __syncthreads();   // previous tile's readers are done with X2
