@@ -176,8 +176,9 @@ struct Args {
     int W, N, c, Kmod, beta;
     int S, lag, nA, nB;
     unsigned long long* log;   // dbg & 16: per-CTA phase timestamps (CTAs < 8, 4096 entries each)
-    int dbg;             // experiment knobs (0 in production): 1 no dependency spin, 2 no global loads,
-                         // 4 no global stores, 8 no DFT arithmetic
+    int dbg;             // experiment knobs (0 in production; results are wrong with 1, 4, 8):
+                         // 1 no dependency spin, 4 no global stores, 8 no DFT arithmetic,
+                         // 16 phase trace (-DNSDGT_TRACE builds)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
