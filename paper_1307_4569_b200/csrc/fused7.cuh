@@ -19,8 +19,8 @@
 // index reversal, so ws is already rotated: pass B needs only E(n).  (Derivation:
 // DESIGN.md §4.3; every identity is exact, the table is built in fp64.)
 //
-// Execution: one persistent launch, CTAs of 128 threads (4 per SM) pull jobs from a global
-// queue.  A job = 8 consecutive columns j of one signal (1 Zak DFT + q product DFTs each),
+// Execution: one persistent launch, CTAs of 128 threads (3 per SM for D = 512, 5 for D = 256)
+// pull jobs from a global queue.  A job = 8 consecutive columns j of one signal (1 Zak DFT + q product DFTs each),
 // B job = 16 consecutive columns n (1 DFT over j each; one 128-byte ring line per row j).
 // Dependencies (B(w) after all A(w); A(w) after all B(w - S) because it reuses ring slot
 // w mod S) are per-slot monotone counters; every job a CTA waits on was dequeued earlier
