@@ -55,8 +55,9 @@ def check(env, L, a, M, l1, l2, g, W, seed, shear=None, expect_fused=True, ncols
     return plan
 
 
-@pytest.mark.parametrize("W", [1, 2, 3, 5, 17, 40])
+@pytest.mark.parametrize("W", [1, 2, 3, 5, 17, 23, 24, 38, 39, 40, 77])
 def test_config3_lattice_small_and_ragged_batches(env, W):
+    """W below, at and above the look-ahead (23) and the ring size (38) of config 3's plan."""
     wl = CONFIGS[2]
     check(env, wl.L, wl.a, wl.M, wl.lam1, wl.lam2, window(wl), W, seed=100 + W)
 

@@ -139,7 +139,7 @@ def test_inverse_errors_and_empty(torch_cuda, nsdgt):
         plan.inverse(torch.zeros((1, M, L // a), dtype=torch.complex128, device="cuda"))
 
 
-@pytest.mark.parametrize("k,W", [(3, 1), (3, 17), (3, 40), (5, 3), (5, 9)])
+@pytest.mark.parametrize("k,W", [(3, 1), (3, 9), (3, 10), (3, 17), (3, 38), (3, 39), (3, 40), (5, 3), (5, 9), (5, 11)])
 def test_fused_synthesis_matches_generic_and_oracle(torch_cuda, nsdgt, oracle_mod, k, W, monkeypatch):
     """Configs 3 and 5 (fused7 lattices): the fused synthesis kernel (fused7_adj.cuh) against
     the generic adjoint kernels on ragged batches, and one signal against the oracle."""
