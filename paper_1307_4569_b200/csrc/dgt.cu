@@ -1409,6 +1409,31 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
     return DGT_OK;
 }
 
+// Arguments of the output kernels (forward and adjoint): intermediate C, coefficients c, the
+// Alg. 1 constants reduced mod 2N / L and the F-branch remap's per-step deltas.
+static OutArgs make_out_args(const Plan* P, void* Cbuf, void* c) {
+    const dgt_lattice_info& I = P->info;
+    OutArgs B{};
+    B.C = Cbuf; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
+    B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
+    B.gscr = P->gB ? P->scrB : nullptr; B.gstride = (int64_t)P->smemB;
+    B.grouped = I.branch == DGT_BRANCH_FREQ ? 1 : 0;
+    B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
+    B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
+    const int64_t twoN = 2 * I.N;
+    auto nm = [](int64_t v, int64_t m) { return ((v % m) + m) % m; };
+    B.C1 = nm(I.C1, twoN); B.C2 = nm(I.C2, twoN); B.C3 = nm(I.C3, twoN); B.C4 = nm(I.C4, twoN);
+    B.C5 = nm(I.C5, twoN); B.C6 = nm(I.C6, I.L);
+    B.sar = (((-(I.s1 % I.L)) * (I.a_r % I.L)) % I.L + I.L) % I.L;
+    B.D1 = (unsigned int)((256 * B.C1) % twoN);
+    B.D5 = (unsigned int)((256 * B.C5) % twoN);
+    B.DX = (unsigned int)(((__int128)256 * B.sar) % I.L);
+    B.invb = (unsigned int)(0xffffffffull / (unsigned long long)I.b);
+    B.inv2N = ~0ull / (unsigned long long)twoN;
+    B.invL = ~0ull / (unsigned long long)I.L;
+    return B;
+}
+
 // F-branch front end for nb signals (Alg. 1 line 23): f^ = fft(pchirp(L, s1) f),
 // unnormalised, into P->fhat (sized for P->fb signals); P_{-s0} is applied on the Zak load.
 // One batched cuFFT call per front batch (config 4: 16 us per signal at batch 16 against
@@ -1477,26 +1502,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     else
         zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->gA ? 0 : P->smemA, st>>>(A);
     prof_close(P, ph, P->zct ? PK_ZAKCT : PK_ZAK, by_in, fl_zak, st);
-    OutArgs B{};
-    B.C = P->Cws; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
-    B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
-    B.gscr = P->gB ? P->scrB : nullptr; B.gstride = (int64_t)P->smemB;
-    B.grouped = I.branch == DGT_BRANCH_FREQ ? 1 : 0;
-    B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
-    B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
-    {
-        const int64_t twoN = 2 * I.N;
-        auto nm = [](int64_t v, int64_t m) { return ((v % m) + m) % m; };
-        B.C1 = nm(I.C1, twoN); B.C2 = nm(I.C2, twoN); B.C3 = nm(I.C3, twoN); B.C4 = nm(I.C4, twoN);
-        B.C5 = nm(I.C5, twoN); B.C6 = nm(I.C6, I.L);
-    }
-    B.sar = (((-(I.s1 % I.L)) * (I.a_r % I.L)) % I.L + I.L) % I.L;
-    B.D1 = (unsigned int)((256 * B.C1) % (2 * I.N));
-    B.D5 = (unsigned int)((256 * B.C5) % (2 * I.N));
-    B.DX = (unsigned int)(((__int128)256 * B.sar) % I.L);
-    B.invb = (unsigned int)(0xffffffffull / (unsigned long long)I.b);
-    B.inv2N = ~0ull / (unsigned long long)(2 * I.N);
-    B.invL = ~0ull / (unsigned long long)I.L;
+    const OutArgs B = make_out_args(P, P->Cws, c);
     const int ntiles = B.grouped ? (int)(I.q * ((I.d + P->NT - 1) / P->NT)) : (int)((I.iN + P->NT - 1) / P->NT);
     ph = prof_open(P, st);
     if (P->outk == 1)
@@ -1671,26 +1677,7 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     using C = cx<T>;
     const dgt_lattice_info& I = P->info;
     const double e = (double)sizeof(C), L = (double)I.L, MN = (double)I.M * (double)I.N;
-    OutArgs B{};
-    B.C = P->Cinv; B.out = const_cast<void*>(c); B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
-    B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
-    B.gscr = P->gB ? P->scrB : nullptr; B.gstride = (int64_t)P->smemB;
-    B.grouped = I.branch == DGT_BRANCH_FREQ ? 1 : 0;
-    B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
-    B.ptab = P->ptab; B.L = I.L; B.b = I.b; B.Nr = I.N_r; B.ar = I.a_r; B.s1 = I.s1;
-    {
-        const int64_t twoN = 2 * I.N;
-        auto nm = [](int64_t v, int64_t m) { return ((v % m) + m) % m; };
-        B.C1 = nm(I.C1, twoN); B.C2 = nm(I.C2, twoN); B.C3 = nm(I.C3, twoN); B.C4 = nm(I.C4, twoN);
-        B.C5 = nm(I.C5, twoN); B.C6 = nm(I.C6, I.L);
-    }
-    B.sar = (((-(I.s1 % I.L)) * (I.a_r % I.L)) % I.L + I.L) % I.L;
-    B.D1 = (unsigned int)((256 * B.C1) % (2 * I.N));
-    B.D5 = (unsigned int)((256 * B.C5) % (2 * I.N));
-    B.DX = (unsigned int)(((__int128)256 * B.sar) % I.L);
-    B.invb = (unsigned int)(0xffffffffull / (unsigned long long)I.b);
-    B.inv2N = ~0ull / (unsigned long long)(2 * I.N);
-    B.invL = ~0ull / (unsigned long long)I.L;
+    const OutArgs B = make_out_args(P, P->Cinv, const_cast<void*>(c));
     const int ntiles = B.grouped ? (int)(I.q * ((I.d + P->NT - 1) / P->NT)) : (int)((I.iN + P->NT - 1) / P->NT);
     int ph = prof_open(P, st);
     if (P->outk == 2)
