@@ -336,3 +336,27 @@ def test_config2_compile_time_zak_matches_runtime(torch_cuda, nsdgt, oracle_mod,
     cols = np.sort(np.random.default_rng(2).choice(wl.N, 16, replace=False))
     ref = oracle_mod.dgt(f, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols)
     assert rel(cc[:, :, torch.from_numpy(cols).cuda()].cpu().numpy(), ref) <= TOL[dtype]
+
+
+def test_two_plans_on_two_streams(torch_cuda, nsdgt):
+    """Distinct plans are independent (include/nsdgt.h): a fused-path plan and a
+    frequency-shear plan executing concurrently on two streams give the results of sequential
+    runs, bit for bit."""
+    torch = torch_cuda
+    wl3, wl4 = CONFIGS[2], CONFIGS[3]
+    p3 = nsdgt.Plan(wl3.L, wl3.a, wl3.M, wl3.lam1, wl3.lam2, window(wl3), dtype="c64")
+    p4 = nsdgt.Plan(wl4.L, wl4.a, wl4.M, wl4.lam1, wl4.lam2, window(wl4), dtype="c128")
+    f3 = torch.from_numpy(batch(wl3, 0, 32)).cuda()
+    f4 = torch.from_numpy(batch(wl4, 0, 2)).cuda()
+    ref3 = p3.execute(f3).clone()
+    ref4 = p4.execute(f4).clone()
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            c3 = p3.execute(f3, stream=s1)
+        with torch.cuda.stream(s2):
+            c4 = p4.execute(f4, stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(c3, ref3) and torch.equal(c4, ref4)
