@@ -360,3 +360,67 @@ def test_two_plans_on_two_streams(torch_cuda, nsdgt):
             c4 = p4.execute(f4, stream=s2)
     torch.cuda.synchronize()
     assert torch.equal(c3, ref3) and torch.equal(c4, ref4)
+
+
+def random_lattices(n, seed=11):
+    """Random feasible lattices with L <= 4096, both branches, p = 1 and p > 1."""
+    from paper_1307_4569_b200 import nsdgt as nd
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        a = int(rng.integers(2, 65))
+        M = int(rng.integers(2, 97))
+        l2 = int(rng.integers(1, 6))
+        l1 = 0 if l2 == 1 else int(rng.integers(1, l2))
+        if math.gcd(l1, l2) != 1:
+            continue
+        lmin = l2 * (a * M // math.gcd(a, M))
+        if lmin > 4096:
+            continue
+        k = int(rng.integers(1, 4096 // lmin + 1))
+        L = lmin * k
+        if L * (L // a) * M > 3_000_000:
+            continue
+        try:
+            nd.lattice_plan(L, a, M, l1, l2)
+        except nd.DgtError:
+            continue
+        out.append((L, a, M, l1, l2))
+    return out
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_random_larger_lattices(torch_cuda, nsdgt, oracle_mod, dtype):
+    """Random feasible lattices up to L = 4096: full comparison with the oracle."""
+    torch = torch_cuda
+    branches = set()
+    for i, (L, a, M, l1, l2) in enumerate(random_lattices(30, seed=11 if dtype == "c128" else 12)):
+        f, g = random_pair(L, 400 + i, dtype=dtype)
+        c, plan = run_gpu(nsdgt, torch, f, g, L, a, M, l1, l2, dtype)
+        branches.add(plan.info["branch"])
+        ref = oracle_mod.dgt(f, g, a, M, l1, l2)
+        assert rel(c, ref) <= TOL[dtype], (L, a, M, l1, l2, plan.info)
+    assert len(branches) >= 2
+
+
+def test_full_size_covariances(torch_cuda, nsdgt):
+    """SURVEY §4 T4 at config 5's full size on the fused path (no oracle): modulation by k
+    channels rolls c along m; translation by x = a lambda2 j samples rolls c along n by
+    lambda2 j with the phase exp(-2 pi i x (m + w(n)) / M)."""
+    torch = torch_cuda
+    wl = CONFIGS[4]
+    g = window(wl)
+    plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c64")
+    f = batch(wl, 0, 1)[0].astype(np.complex128)
+    l = np.arange(wl.L)
+    k, j = 5, 3
+    b = wl.L // wl.M
+    x = wl.a * wl.lam2 * j
+    fs = np.stack([f, f * np.exp(2j * np.pi * b * k * l / wl.L), np.roll(f, x)]).astype(np.complex64)
+    c = plan.execute(torch.from_numpy(fs).cuda()).cpu().numpy().astype(np.complex128)
+    assert rel(c[1], np.roll(c[0], k, axis=0)) <= 5e-5
+    m = np.arange(wl.M)[:, None]
+    n = np.arange(wl.N)[None, :]
+    wn = ((n * wl.lam1) % wl.lam2) / wl.lam2
+    ph = np.exp(-2j * np.pi * x * (m + wn) / wl.M)
+    assert rel(c[2], ph * np.roll(c[0], wl.lam2 * j, axis=1)) <= 5e-5
