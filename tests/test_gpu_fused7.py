@@ -145,3 +145,17 @@ def test_real_input_on_fused_lattice(env):
     assert rel(cr, cc) <= TOL
     cols = np.arange(0, wl.N, 97)
     assert rel(cr[:, :, cols], oracle.dgt(f, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols)) <= TOL
+
+
+def test_shard_results_bitwise_equal(env):
+    """SURVEY §4 T6 on one GPU: a batch split into shards (what each rank of a multi-GPU run
+    transforms) gives bit-for-bit the coefficients of the whole batch -- the per-signal
+    arithmetic does not depend on W or on the ring slot."""
+    torch, nsdgt, _ = env
+    for k, W in ((5, 8), (3, 40)):
+        wl = CONFIGS[k - 1]
+        plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, window(wl), dtype="c64")
+        ft = torch.from_numpy(signals(wl.L, W, 900 + k)).cuda()
+        whole = plan.execute(ft)
+        parts = [plan.execute(ft[i:i + W // 4].contiguous()) for i in range(0, W, W // 4)]
+        assert torch.equal(whole, torch.cat(parts)), k
