@@ -303,9 +303,15 @@ def main():
     coefs_per_step = wl.W * wl.M * wl.N
     value = coefs_per_step / (ms_per_step * 1e-3)
 
-    # roofline of the dominant kernel (largest summed duration)
+    # roofline of the dominant kernel (largest summed duration): SURVEY 8(d)'s algorithmic bytes
+    # per signal (input + coefficients, window once) x the signals one launch of that kernel
+    # processes (a multi-kernel path -- config 4's cuFFT / zak_ct / out_f4096 -- runs each kernel
+    # once per chunk of signals; intermediates are not algorithmic)
+    step_bytes = Wr * (wl.L * (8 if wl.dtype == "c64" else 16) // (2 if wl.real_input else 1)
+                       + wl.M * wl.N * (8 if wl.dtype == "c64" else 16)) + wl.L * (8 if wl.dtype == "c64" else 16)
     dom = max(stats, key=lambda s: s["ms"])
-    per_launch_bytes = dom["bytes"] / dom["launches"]
+    launches_per_step = dom["launches"] / args.steps
+    per_launch_bytes = step_bytes / launches_per_step
     per_launch_ms = dom["ms"] / dom["launches"]
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
@@ -316,8 +322,6 @@ def main():
                 "kernel_share_of_step": dom["ms"] / ms_total if ms_total > 0 else None,
                 "model_tflops": dom["flops"] / (dom["ms"] * 1e-3) / 1e12,
                 "kernels": stats}
-    step_bytes = Wr * (wl.L * (8 if wl.dtype == "c64" else 16) // (2 if wl.real_input else 1)
-                       + wl.M * wl.N * (8 if wl.dtype == "c64" else 16)) + wl.L * (8 if wl.dtype == "c64" else 16)
     step_gbs = step_bytes / (ms_total / args.steps * 1e-3) / 1e9
 
     # end to end through the C ABI with HOST buffers (pinned), copies inside the timed region

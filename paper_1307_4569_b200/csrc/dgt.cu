@@ -204,6 +204,7 @@ struct ZakArgs {
     int64_t gstride;       // bytes per CTA in gscr
     Radices rd;
     const void* tw;     // twiddles of length d
+    int cnj;            // zak_ct only: intermediate stored [W][n][iM] (n = kappa + q n', j fastest)
 };
 
 template <typename T>
@@ -390,6 +391,23 @@ __global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
     C* Y = fft_ct<T, D>(Yb, phi, Q * RBC, tw);   // Phi is dead: its buffer is the scratch
     C* Cw = (C*)A.C + w * A.iM * Q * D;
     const int jbase = r0 + c * (l % Q);
+    if (A.cnj) {
+        // [n][j] layout: rr fastest, RBC consecutive j per (kappa, n') (RBC * e = 64 B runs)
+        const int iM = (int)A.iM;
+#pragma unroll
+        for (int it = 0; it < NP; ++it) {
+            const int i = tid + it * NT;
+            if (i < Q * RBC * D) {
+                const int u = i / (RBC * D), rem = i % (RBC * D);
+                const int np = rem / RBC, rr = rem % RBC;
+                const int kappa = (l - u + Q) % Q;
+                int tau = D - np - (l < u ? 1 : 0);
+                if (tau >= D) tau -= D;
+                Cw[(int64_t)(kappa + Q * np) * iM + jbase + rr] = Y[(u * RBC + rr) * D + tau];
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int it = 0; it < NP; ++it) {
         const int i = tid + it * NT;
@@ -414,6 +432,7 @@ struct OutArgs {
     int grouped;    // 1: CTA x = (kappa, block of NT consecutive n'), contiguous loads
     Radices rd;
     const void* tw;  // twiddles of length iM
+    int cnj;         // out_f4096 only: intermediate stored [W][n][iM] (see ZakArgs::cnj)
     int branch;
     // T-branch
     const void* E;
@@ -649,9 +668,10 @@ __global__ void __launch_bounds__(256, MINB) out_f4096_kernel(OutArgs A) {
     const int m = blockIdx.x;              // inner column
     const int64_t w = blockIdx.y;
     const int qi = (int)A.q, di = (int)A.d;
-    const C* __restrict__ src = (const C*)A.C + w * A.iM * A.iN + (m % qi) * di + m / qi;
+    const C* __restrict__ src = (const C*)A.C + w * A.iM * A.iN +
+                                (A.cnj ? (int64_t)m * A.iM : (int64_t)((m % qi) * di + m / qi));
     const C* __restrict__ tw = (const C*)A.tw;
-    const int ld = qi * di;                // row stride of C over j
+    const int ld = A.cnj ? 1 : qi * di;    // stride of C over j
     C v[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = src[(tid + 256 * r) * ld];
@@ -836,8 +856,8 @@ __global__ void __launch_bounds__(256, MINB) out_f4096_adj_kernel(OutArgs A) {
 #pragma unroll
     for (int t1 = 0; t1 < 16; ++t1) v[t1] = S[hi * 272 + 17 * lo + t1];
     dft16<T>(v);
-    C* dst = (C*)A.C + w * A.iM * A.iN + (m % qi) * di + m / qi;
-    const int ld = qi * di;
+    C* dst = (C*)A.C + w * A.iM * A.iN + (A.cnj ? (int64_t)m * A.iM : (int64_t)((m % qi) * di + m / qi));
+    const int ld = A.cnj ? 1 : qi * di;
 #pragma unroll
     for (int k3 = 0; k3 < 16; ++k3) dst[(hi + 16 * lo + 256 * k3) * ld] = mk<T>(v[k3].x, -v[k3].y);
 }
@@ -862,14 +882,18 @@ __global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fou
     {
         const C* Cw = (const C*)A.C + w * A.iM * Q * D;
         const int jbase = r0 + c * (l % Q);
+        const bool cnj = A.cnj != 0;   // [n][j] layout: rr fastest (see zak_ct_kernel)
+        const int iM = (int)A.iM;
         C v[NP];
 #pragma unroll
         for (int it = 0; it < NP; ++it) {
             const int i = tid + it * NT;
             if (i < Q * RBC * D) {
                 const int u = i / (RBC * D), rem = i % (RBC * D);
-                const int rr = rem / D, np = rem % D;
-                v[it] = Cw[((jbase + rr) * Q + (l - u + Q) % Q) * D + np];
+                const int rr = cnj ? rem % RBC : rem / D, np = cnj ? rem / RBC : rem % D;
+                const int kappa = (l - u + Q) % Q;
+                v[it] = cnj ? Cw[(int64_t)(kappa + Q * np) * iM + jbase + rr]
+                            : Cw[((jbase + rr) * Q + kappa) * D + np];
             }
         }
 #pragma unroll
@@ -877,7 +901,7 @@ __global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fou
             const int i = tid + it * NT;
             if (i < Q * RBC * D) {
                 const int u = i / (RBC * D), rem = i % (RBC * D);
-                const int rr = rem / D, np = rem % D;
+                const int rr = cnj ? rem % RBC : rem / D, np = cnj ? rem / RBC : rem % D;
                 int tau = D - np - (l < u ? 1 : 0);
                 if (tau >= D) tau -= D;
                 R1[(u * RBC + rr) * D + tau] = mk<T>(v[it].x, -v[it].y);
@@ -1224,6 +1248,7 @@ struct Plan {
     int zct = 0;             // zak_kernel compile-time inner length (0 = runtime radices)
     int inv_generic = 0;     // experiment knob (NSDGT_INV_GENERIC, read at plan time): generic synthesis
     int outct = 0;           // out_kernel compile-time inner channel count (0 = runtime radices)
+    int cnj = 0;             // zak_ct -> out_f4096 intermediate in [n][j] layout
     int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
     int fast = 0;  // specialised path id (0 = generic)
     FastPlan fp{};
@@ -1415,7 +1440,7 @@ static OutArgs make_out_args(const Plan* P, void* Cbuf, void* c) {
     const dgt_lattice_info& I = P->info;
     OutArgs B{};
     B.C = Cbuf; B.out = c; B.iM = I.iM; B.iN = I.iN; B.q = I.q; B.d = I.d; B.NT = P->NT;
-    B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch;
+    B.rd = P->rd_m; B.tw = P->tw_m; B.branch = (int)I.branch; B.cnj = P->cnj;
     B.gscr = P->gB ? P->scrB : nullptr; B.gstride = (int64_t)P->smemB;
     B.grouped = I.branch == DGT_BRANCH_FREQ ? 1 : 0;
     B.E = P->E; B.rot = P->rot; B.M = I.M; B.N = I.N;
@@ -1489,7 +1514,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     ZakArgs A{};
     A.f = src; A.real_in = real_src; A.chirp = P->chirp; A.G = P->G; A.C = P->Cws;
     A.L = I.L; A.c = I.c; A.d = I.d; A.p = I.p; A.q = I.q; A.iM = I.iM;
-    A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = P->allu;
+    A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = P->allu; A.cnj = P->cnj;
     A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
@@ -1603,6 +1628,9 @@ static int configure(Plan* P, int64_t max_chunk) {
     // registers with spills), 3 for c64
     P->outk = (I.branch == DGT_BRANCH_FREQ && I.iM == 4096 && !std::getenv("NSDGT_OUT_GENERIC")) ? (e == 16 ? 2 : 1) : 0;
     if (P->outk && std::getenv("NSDGT_OUTF_MINB")) P->outk = std::atoi(std::getenv("NSDGT_OUTF_MINB")) == 2 ? 2 : 1;   // experiment
+    // zak_ct (d = 180) feeding out_f4096: the intermediate is stored [n][j] so the output
+    // kernel's column loads are contiguous (NSDGT_CNJ_OFF: the generic [j][kappa][n'] layout)
+    P->cnj = (P->outk && P->zct == 180 && !std::getenv("NSDGT_CNJ_OFF")) ? 1 : 0;
     CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kOutF4096Elems * e)));
     CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1690,7 +1718,7 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     ZakArgs A{};
     A.f = nullptr; A.real_in = 0; A.chirp = P->chirp; A.G = P->G; A.C = P->Cinv;
     A.L = I.L; A.c = I.c; A.d = I.d; A.p = I.p; A.q = I.q; A.iM = I.iM;
-    A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = 0;
+    A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = 0; A.cnj = P->cnj;
     A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     const bool freq = I.branch == DGT_BRANCH_FREQ;

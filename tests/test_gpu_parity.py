@@ -204,6 +204,26 @@ def test_config4_lattice_c64_sampled(torch_cuda, nsdgt, oracle_mod):
     assert rel(got, ref) <= TOL["c64"]
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_config4_intermediate_layouts_bitwise_equal(torch_cuda, nsdgt, dtype, monkeypatch):
+    """zak_ct -> out_f4096 on config 4 store the intermediate [n][j] (contiguous output-kernel
+    loads); the generic [j][kappa][n'] layout (NSDGT_CNJ_OFF) runs the same arithmetic, so
+    analysis and synthesis are bit-for-bit equal between the two layouts."""
+    torch = torch_cuda
+    wl = CONFIGS[3]
+    g = window(wl)
+    f = torch.from_numpy(batch(wl, 0, 3).astype(np.complex64 if dtype == "c64" else np.complex128)).cuda()
+    p1 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
+    c1 = p1.execute(f)
+    r1 = p1.inverse(c1)
+    monkeypatch.setenv("NSDGT_CNJ_OFF", "1")
+    p0 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
+    c0 = p0.execute(f)
+    r0 = p0.inverse(c0)
+    assert torch.equal(c1, c0)
+    assert torch.equal(r1, r0)
+
+
 def test_chunking_ragged_and_host_path(torch_cuda, nsdgt):
     """Ragged chunks (W not a multiple of the chunk), W = 0, and the host end-to-end path
     give bitwise the same result as one device execute."""

@@ -13,6 +13,8 @@ echo done
 for k in 2 3 4; do python bench.py --config $k --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg${k}_$tag.json 2>/dev/null; done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg4_$tag.csv python bench.py --config 4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"zak|out_f4096" -s 2 -c 2 -o gpurun_out/prof_cfg4_$tag python bench.py --config 4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:fused7 -s 1 -c 1 -o gpurun_out/prof_cfg3_$tag python bench.py --config 3 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:adj -s 2 -c 2 -o gpurun_out/prof_inv_cfg4_$tag python bench.py --config 4 --inverse --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 echo done2
 for k in 5 3 4 2; do python bench.py --config $k --inverse --steps 10 --warmup 3 --cpu-budget 5 > gpurun_out/bench_inv_cfg${k}_$tag.json 2>/dev/null; done
 ncu --set full --clock-control none --import-source on -k regex:fused7a -s 1 -c 1 -o gpurun_out/prof_inv_$tag python bench.py --inverse --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
