@@ -322,11 +322,24 @@ __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
 // sequences, scatter), but every index divides by a constant, each thread issues all its
 // global loads of a phase before using them, and p = 1 makes the gather index
 // z = l + Q s < L/c (no reduction).
-template <typename T, int D, int Q, int RBC>
-__global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
+// Row order of zak_ct's RBC-column loops: rows (stride D in shared memory) are visited in
+// aligned blocks of 8 with the upper half of the columns shifted by 2 rows, so one shared-memory
+// wavefront (4 x 16-byte or 8 x 8-byte columns, 2 rows) hits distinct banks -- D e / 16 B is
+// 4 mod 8 for d = 180, which made column c and c + RBC/2 collide.  A permutation within each
+// block (ragged last block unchanged); the global side still moves RBC consecutive elements.
+template <int D, int RBC, int E>
+__device__ __forceinline__ int zrow(int g, int rr, int G) {
+    if constexpr (RBC * E == 64 && D % 8 == 4)
+        return (g | 7) < G ? ((g & ~7) | ((g + 2 * (rr / (RBC / 2))) & 7)) : g;
+    else
+        return g;
+}
+
+template <typename T, int D, int Q, int RBC, int NT = 256>
+__global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
-    constexpr int NT = 256, NG = (RBC * D + NT - 1) / NT, NP = (Q * RBC * D + NT - 1) / NT;
+    constexpr int NG = (RBC * D + NT - 1) / NT, NP = (Q * RBC * D + NT - 1) / NT;
     const int c = (int)A.c;
     const int nrb = c / RBC;
     const int rblk = blockIdx.x % nrb, l = blockIdx.x / nrb;
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
         for (int it = 0; it < NG; ++it) {
             const int i = tid + it * NT;
             if (i < RBC * D) {
-                const int rr = i % RBC, s = i / RBC;
+                const int rr = i % RBC, s = zrow<D, RBC, sizeof(C)>(i / RBC, rr, D);
                 const int x = r0 + rr + c * (l + Q * s);
                 v[it] = A.real_in ? mk<T>(fr[x], T(0)) : fc[x];
             }
@@ -356,7 +369,7 @@ __global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
             for (int it = 0; it < NG; ++it) {
                 const int i = tid + it * NT;
                 if (i < RBC * D) {
-                    const int rr = i % RBC, s = i / RBC;
+                    const int rr = i % RBC, s = zrow<D, RBC, sizeof(C)>(i / RBC, rr, D);
                     v[it] = cmul(v[it], __ldg(chirp + r0 + rr + c * (l + Q * s)));
                 }
             }
@@ -364,7 +377,7 @@ __global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
 #pragma unroll
         for (int it = 0; it < NG; ++it) {
             const int i = tid + it * NT;
-            if (i < RBC * D) R1[(i % RBC) * D + i / RBC] = v[it];
+            if (i < RBC * D) R1[(i % RBC) * D + zrow<D, RBC, sizeof(C)>(i / RBC, i % RBC, D)] = v[it];
         }
     }
     __syncthreads();
@@ -398,8 +411,8 @@ __global__ void __launch_bounds__(256, 2) zak_ct_kernel(ZakArgs A) {
         for (int it = 0; it < NP; ++it) {
             const int i = tid + it * NT;
             if (i < Q * RBC * D) {
-                const int u = i / (RBC * D), rem = i % (RBC * D);
-                const int np = rem / RBC, rr = rem % RBC;
+                const int rr = i % RBC, g = zrow<D, RBC, sizeof(C)>(i / RBC, rr, Q * D);
+                const int u = g / D, np = g % D;
                 const int kappa = (l - u + Q) % Q;
                 int tau = D - np - (l < u ? 1 : 0);
                 if (tau >= D) tau -= D;
@@ -865,11 +878,11 @@ __global__ void __launch_bounds__(256, MINB) out_f4096_adj_kernel(OutArgs A) {
 // Adjoint of zak_ct_kernel (d = D, q = Q, RBC columns): gather conj(T'_u(tau)) for all u
 // through the inverse scatter map, one DFT_D of Q RBC sequences, conj(Phi')(nu) =
 // sum_u Y_u(nu) G_u(nu), one DFT_D of the RBC columns, f(x) = conj(chirp(x) R(s)).
-template <typename T, int D, int Q, int RBC>
-__global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fout) {
+template <typename T, int D, int Q, int RBC, int NT = 256>
+__global__ void __launch_bounds__(NT, 512 / NT) zak_ct_adj_kernel(ZakArgs A, void* fout) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
-    constexpr int NT = 256, NG = (RBC * D + NT - 1) / NT, NP = (Q * RBC * D + NT - 1) / NT;
+    constexpr int NG = (RBC * D + NT - 1) / NT, NP = (Q * RBC * D + NT - 1) / NT;
     const int c = (int)A.c;
     const int nrb = c / RBC;
     const int rblk = blockIdx.x % nrb, l = blockIdx.x / nrb;
@@ -889,8 +902,9 @@ __global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fou
         for (int it = 0; it < NP; ++it) {
             const int i = tid + it * NT;
             if (i < Q * RBC * D) {
-                const int u = i / (RBC * D), rem = i % (RBC * D);
-                const int rr = cnj ? rem % RBC : rem / D, np = cnj ? rem / RBC : rem % D;
+                const int g = zrow<D, RBC, sizeof(C)>(i / RBC, i % RBC, Q * D);
+                const int u = cnj ? g / D : i / (RBC * D), rem = i % (RBC * D);
+                const int rr = cnj ? i % RBC : rem / D, np = cnj ? g % D : rem % D;
                 const int kappa = (l - u + Q) % Q;
                 v[it] = cnj ? Cw[(int64_t)(kappa + Q * np) * iM + jbase + rr]
                             : Cw[((jbase + rr) * Q + kappa) * D + np];
@@ -900,8 +914,9 @@ __global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fou
         for (int it = 0; it < NP; ++it) {
             const int i = tid + it * NT;
             if (i < Q * RBC * D) {
-                const int u = i / (RBC * D), rem = i % (RBC * D);
-                const int rr = cnj ? rem % RBC : rem / D, np = cnj ? rem / RBC : rem % D;
+                const int g = zrow<D, RBC, sizeof(C)>(i / RBC, i % RBC, Q * D);
+                const int u = cnj ? g / D : i / (RBC * D), rem = i % (RBC * D);
+                const int rr = cnj ? i % RBC : rem / D, np = cnj ? g % D : rem % D;
                 int tau = D - np - (l < u ? 1 : 0);
                 if (tau >= D) tau -= D;
                 R1[(u * RBC + rr) * D + tau] = mk<T>(v[it].x, -v[it].y);
@@ -934,7 +949,7 @@ __global__ void __launch_bounds__(256, 2) zak_ct_adj_kernel(ZakArgs A, void* fou
     for (int it = 0; it < NG; ++it) {
         const int i = tid + it * NT;
         if (i < RBC * D) {
-            const int rr = i % RBC, s = i / RBC;   // rr fastest: RBC consecutive residues per row s
+            const int rr = i % RBC, s = zrow<D, RBC, sizeof(C)>(i / RBC, rr, D);   // rr fastest (RBC consecutive residues per row s)
             const int x = r0 + rr + c * (l + Q * s);
             C v = R[rr * D + s];
             if (chirp) v = cmul(v, __ldg(chirp + x));
@@ -1248,6 +1263,7 @@ struct Plan {
     int zct = 0;             // zak_kernel compile-time inner length (0 = runtime radices)
     int inv_generic = 0;     // experiment knob (NSDGT_INV_GENERIC, read at plan time): generic synthesis
     int outct = 0;           // out_kernel compile-time inner channel count (0 = runtime radices)
+    int zsmall = 0;          // forward zak_ct with 128-thread CTAs of RB / 2 columns (c128, d = 180)
     int cnj = 0;             // zak_ct -> out_f4096 intermediate in [n][j] layout
     int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
     int fast = 0;  // specialised path id (0 = generic)
@@ -1518,7 +1534,9 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
-    if (P->zct == 180 && sizeof(C) == 16)
+    if (P->zsmall && sizeof(C) == 16)
+        zak_ct_kernel<T, 180, 4, 2, 128><<<dim3(2 * nrb * (unsigned)I.q, (unsigned)Wc), 128, P->smemA / 2, st>>>(A);
+    else if (P->zct == 180 && sizeof(C) == 16)
         zak_ct_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     else if (P->zct == 180)
         zak_ct_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
@@ -1595,6 +1613,10 @@ static int configure(Plan* P, int64_t max_chunk) {
     if (P->allu && I.q == 4 && I.c % P->RB == 0 && !std::getenv("NSDGT_ZAK_RT")) {
         if (I.d == 180 && P->RB == (int)(64 / e)) P->zct = 180;
         if (I.d == 720 && P->RB == 1) P->zct = 720;
+        // c128 forward: 128-thread CTAs of RB / 2 columns (32-byte rows), 4 CTAs per SM -- finer
+        // barriers than 2 CTAs of 8 warps (config 4: 0.497 -> 0.474 ms per 16 signals); the
+        // adjoint measured slower that way (0.492 -> 0.527) and keeps RB
+        P->zsmall = (P->zct == 180 && e == 16 && !std::getenv("NSDGT_ZCT_BIG")) ? 1 : 0;
     }
     if (P->zct) {
         // the constant-memory twiddles of fft_ct (same values for every plan; long-double
@@ -1619,6 +1641,7 @@ static int configure(Plan* P, int64_t max_chunk) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 720, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
+        CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA / 2));
     }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     // compile-time output DFT for M' = 200 (config 2, time shear)

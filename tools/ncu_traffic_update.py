@@ -1,7 +1,7 @@
 """Record per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the kernels in
 an `ncu --set full` report into profiles/ncu_traffic.json under a workload name, keyed by the
 profile-kind names bench.py reports (tools only).
-usage: python tools/ncu_traffic_update.py REPORT.ncu-rep WORKLOAD"""
+usage: python tools/ncu_traffic_update.py REPORT.ncu-rep|RAW.csv WORKLOAD"""
 import csv
 import io
 import json
@@ -24,7 +24,10 @@ def to_bytes(v, unit):
 
 def main():
     rep, workload = sys.argv[1], sys.argv[2]
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):   # a raw page exported on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units = rows[0], rows[1]
     path = os.path.join(os.path.dirname(__file__), "..", "profiles", "ncu_traffic.json")

@@ -19,4 +19,9 @@ echo done2
 for k in 5 3 4 2; do python bench.py --config $k --inverse --steps 10 --warmup 3 --cpu-budget 5 > gpurun_out/bench_inv_cfg${k}_$tag.json 2>/dev/null; done
 ncu --set full --clock-control none --import-source on -k regex:fused7a -s 1 -c 1 -o gpurun_out/prof_inv_$tag python bench.py --inverse --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref_$tag.json 2>/dev/null
+# export the raw pages (small) and keep only the config-5 fused7 report (gpurun copies back <= 64 MiB)
+for r in gpurun_out/prof_*$tag.ncu-rep; do ncu -i $r --page raw --csv > ${r%.ncu-rep}_raw.csv 2>/dev/null; done
+ncu -i gpurun_out/prof_$tag.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/prof_${tag}_source.csv 2>/dev/null
+for r in gpurun_out/prof_*$tag.ncu-rep; do [ "$r" = "gpurun_out/prof_$tag.ncu-rep" ] || rm -f $r; done
+du -sh gpurun_out
 echo done3
