@@ -159,10 +159,14 @@ class Plan:
             g_t = g_np
             gptr = g_np.ctypes.data
             flags |= DGT_G_ON_HOST
+        ng = int(g_t.numel()) if isinstance(g_t, torch.Tensor) else int(g_t.size)
+        if (fir and not 0 < ng <= L) or (not fir and ng != L):
+            raise ValueError(f"window has {ng} samples; the plan needs {'1..L' if fir else 'L'} = {L}")
+        self._device = torch.cuda.current_device() if torch.cuda.is_available() else -1
         s0, s1 = shear if shear is not None else (0, 0)
         h = ctypes.c_void_p()
         if fir:
-            Lg = int(g_t.shape[0]) if not isinstance(g_t, np.ndarray) else int(g_t.size)
+            Lg = ng
             _check(_lib.dgt_plan_fir(ctypes.byref(h), L, a, M, lam1, lam2, ctypes.c_void_p(gptr), Lg, int(Lb), code,
                                      flags, _stream_ptr(stream)), "dgt_plan_fir")
         else:
@@ -203,6 +207,10 @@ class Plan:
         return [{"name": stats[i].name.decode(), "launches": int(stats[i].launches), "ms": float(stats[i].ms),
                  "bytes": float(stats[i].bytes), "flops": float(stats[i].flops)} for i in range(min(n.value, 16))]
 
+    def _check_device(self, t):
+        if t.device.index != self._device:
+            raise ValueError(f"tensor on {t.device}, plan built on cuda:{self._device}")
+
     def execute(self, f, out=None, stream=None):
         """c[W, M, N] (CUDA tensor) = DGT of f[W, L] (CUDA tensor); 1-D f gives c[M, N]."""
         import torch
@@ -214,11 +222,13 @@ class Plan:
         if f2.dtype != want or not f2.is_contiguous():
             raise TypeError(f"f must be a contiguous {want} tensor of shape (W, L)")
         W = f2.shape[0]
-        if f2.shape[1] != self.L:
+        if f2.dim() != 2 or f2.shape[1] != self.L:
             raise ValueError("f has the wrong length")
+        self._check_device(f2)
         if out is None:
             out = torch.empty((W, self.M, self.N), dtype=self._cdt, device=f.device)
-        elif out.dtype != self._cdt or not out.is_contiguous() or out.numel() != W * self.M * self.N:
+        elif (out.dtype != self._cdt or not out.is_contiguous() or out.numel() != W * self.M * self.N
+              or out.device != f2.device):
             raise TypeError("bad output tensor")
         _check(_lib.dgt_execute(self._h, ctypes.c_void_p(f2.data_ptr()), ctypes.c_void_p(out.data_ptr()), W,
                                 _stream_ptr(stream)), "dgt_execute")
@@ -236,9 +246,10 @@ class Plan:
         if c2.dtype != self._cdt or not c2.is_contiguous() or tuple(c2.shape[1:]) != (self.M, self.N):
             raise TypeError(f"c must be a contiguous {self._cdt} tensor of shape (W, M, N)")
         W = c2.shape[0]
+        self._check_device(c2)
         if out is None:
             out = torch.empty((W, self.L), dtype=self._cdt, device=c.device)
-        elif out.dtype != self._cdt or not out.is_contiguous() or out.numel() != W * self.L:
+        elif out.dtype != self._cdt or not out.is_contiguous() or out.numel() != W * self.L or out.device != c2.device:
             raise TypeError("bad output tensor")
         _check(_lib.dgt_execute_inverse(self._h, ctypes.c_void_p(c2.data_ptr()), ctypes.c_void_p(out.data_ptr()), W,
                                         _stream_ptr(stream)), "dgt_execute_inverse")
@@ -255,21 +266,35 @@ class Plan:
     def execute_host(self, f, out=None, stream=None):
         """End-to-end call on HOST arrays (numpy or CPU tensors; pinned memory is faster)."""
         import torch
-        squeeze = False
+        want = self._rdt if self.real_input else self._cdt
         if isinstance(f, torch.Tensor):
+            if f.is_cuda:
+                raise TypeError("execute_host() takes host arrays; use execute() for CUDA tensors")
             squeeze = f.dim() == 1
             f2 = f.reshape(1, -1) if squeeze else f
+            if f2.dtype != want or not f2.is_contiguous() or f2.dim() != 2 or f2.shape[1] != self.L:
+                raise TypeError(f"f must be a contiguous {want} CPU tensor of shape (W, L)")
             fptr, W = f2.data_ptr(), f2.shape[0]
             if out is None:
                 out = torch.empty((W, self.M, self.N), dtype=self._cdt, pin_memory=f2.is_pinned())
+            elif (out.is_cuda or out.dtype != self._cdt or not out.is_contiguous()
+                  or out.numel() != W * self.M * self.N):
+                raise TypeError("bad output tensor")
             optr = out.data_ptr()
         else:
+            np_want = np.dtype(str(want).replace("torch.", ""))
             f_np = np.asarray(f)
             squeeze = f_np.ndim == 1
-            f2 = np.ascontiguousarray(np.atleast_2d(f_np))
+            f2 = np.ascontiguousarray(np.atleast_2d(f_np), dtype=np_want)
+            if f2.ndim != 2 or f2.shape[1] != self.L:
+                raise ValueError(f"f must have shape (W, {self.L})")
             fptr, W = f2.ctypes.data, f2.shape[0]
+            np_c = np.complex64 if self.dtype == "c64" else np.complex128
             if out is None:
-                out = np.empty((W, self.M, self.N), dtype=np.complex64 if self.dtype in ("c64",) else np.complex128)
+                out = np.empty((W, self.M, self.N), dtype=np_c)
+            elif (out.dtype != np_c or not out.flags.c_contiguous or out.size != W * self.M * self.N
+                  or not out.flags.writeable):
+                raise TypeError("bad output array")
             optr = out.ctypes.data
         _check(_lib.dgt_execute_host(self._h, ctypes.c_void_p(fptr), ctypes.c_void_p(optr), W, _stream_ptr(stream)),
                "dgt_execute_host")

@@ -288,6 +288,31 @@ def test_errors_on_gpu(torch_cuda, nsdgt):
         plan.execute(torch.zeros(48, dtype=torch.complex128, device="cuda"))
 
 
+def test_binding_argument_checks(torch_cuda, nsdgt):
+    """The ctypes binding validates what the C ABI cannot see (buffer lengths, dtypes, devices)
+    before passing raw pointers: wrong window length, wrong host dtype / shape, bad outputs."""
+    torch = torch_cuda
+    L, a, M = 48, 4, 6
+    with pytest.raises(ValueError):
+        nsdgt.Plan(L, a, M, 1, 2, np.ones(L - 1), dtype="c64")   # would read past the window
+    plan = nsdgt.Plan(L, a, M, 1, 2, np.ones(L), dtype="c128")
+    f = np.random.default_rng(3).standard_normal((2, L)) + 0j
+    ref = plan.execute(torch.from_numpy(f).cuda()).cpu().numpy()
+    # numpy input is converted to the plan's dtype; torch input must match exactly
+    assert np.array_equal(plan.execute_host(f), ref)
+    assert np.allclose(plan.execute_host(f.astype(np.complex64)), ref, atol=1e-5)
+    with pytest.raises(TypeError):
+        plan.execute_host(torch.from_numpy(f.astype(np.complex64)))   # c64 data, c128 plan
+    with pytest.raises(TypeError):
+        plan.execute_host(torch.from_numpy(f).cuda())
+    with pytest.raises(ValueError):
+        plan.execute_host(np.zeros((2, L + 1), dtype=np.complex128))
+    with pytest.raises(TypeError):
+        plan.execute_host(f, out=np.zeros((2, M, L // a), dtype=np.complex64))
+    with pytest.raises(TypeError):
+        plan.execute(torch.from_numpy(f).cuda(), out=torch.zeros((1, M, L // a), dtype=torch.complex128, device="cuda"))
+
+
 FIG2 = [(a, M, lam2) for a, M in [(32, 64), (40, 60), (60, 80)] for lam2 in (1, 2, 3, 5, 7, 10)]
 
 
