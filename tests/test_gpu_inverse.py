@@ -129,6 +129,29 @@ def test_adjointness_on_gpu(torch_cuda, nsdgt):
     assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_adjointness_random_midsize_lattices(torch_cuda, nsdgt, dtype):
+    """<dgt(f), c> = <f, idgt(c)> on random lattices with L up to 2^18 (the forward map on these
+    lattices is oracle-checked in test_gpu_parity.py::test_random_midsize_lattices_sampled), so
+    the synthesis kernels are pinned there through the adjoint identity."""
+    import math
+    torch = torch_cuda
+    from test_gpu_parity import random_midsize_lattices
+    tol = 1e-11 if dtype == "c128" else 2e-5
+    for i, (L, a, M, l1, l2) in enumerate(random_midsize_lattices(8, seed=31 if dtype == "c128" else 32)):
+        f, g = random_pair(L, 900 + i, dtype=dtype)
+        rng = np.random.default_rng(i)
+        c = rand_c(rng, 1, M, L // a, dtype)
+        plan = nsdgt.Plan(L, a, M, l1, l2, g, dtype=dtype)
+        cf = plan.execute(torch.from_numpy(f[None]).cuda()).cpu().numpy().astype(np.complex128)
+        fi = plan.inverse(torch.from_numpy(c).cuda()).cpu().numpy().astype(np.complex128)
+        lhs = np.vdot(c.astype(np.complex128), cf)
+        rhs = np.vdot(fi, f[None].astype(np.complex128))
+        scale = np.linalg.norm(c) * np.linalg.norm(cf)
+        assert abs(lhs - rhs) <= tol * scale, (L, a, M, l1, l2, abs(lhs - rhs) / scale)
+        assert math.isfinite(abs(lhs))
+
+
 def test_inverse_errors_and_empty(torch_cuda, nsdgt):
     torch = torch_cuda
     L, a, M = 48, 4, 6

@@ -448,6 +448,51 @@ def test_random_larger_lattices(torch_cuda, nsdgt, oracle_mod, dtype):
     assert len(branches) >= 2
 
 
+def random_midsize_lattices(n, seed):
+    """Random feasible lattices with 4096 < L <= 2^18 (a, M up to 256, lambda2 up to 7)."""
+    from paper_1307_4569_b200 import nsdgt as nd
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        a = int(rng.integers(2, 257))
+        M = int(rng.integers(2, 257))
+        l2 = int(rng.integers(1, 8))
+        l1 = 0 if l2 == 1 else int(rng.integers(1, l2))
+        if math.gcd(l1, l2) != 1 or a >= M * 4:
+            continue
+        lmin = l2 * (a * M // math.gcd(a, M))
+        if lmin > (1 << 18):
+            continue
+        ks = [k for k in range(1, (1 << 18) // lmin + 1) if lmin * k > 4096]
+        if not ks:
+            continue
+        L = lmin * int(rng.choice(ks))
+        try:
+            nd.lattice_plan(L, a, M, l1, l2)
+        except nd.DgtError:
+            continue
+        out.append((L, a, M, l1, l2))
+    return out
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_random_midsize_lattices_sampled(torch_cuda, nsdgt, oracle_mod, dtype):
+    """Random feasible lattices with L up to 2^18 (beyond the full-comparison sweep): two
+    signals per lattice, 8 sampled columns against the oracle, both shear branches."""
+    torch = torch_cuda
+    branches = set()
+    for i, (L, a, M, l1, l2) in enumerate(random_midsize_lattices(14, seed=21 if dtype == "c128" else 22)):
+        f1, g = random_pair(L, 700 + i, dtype=dtype)
+        f2, _ = random_pair(L, 800 + i, dtype=dtype)
+        f = np.stack([f1, f2])
+        c, plan = run_gpu(nsdgt, torch, f, g, L, a, M, l1, l2, dtype)
+        branches.add(plan.info["branch"])
+        cols = np.sort(np.random.default_rng(i).choice(L // a, min(8, L // a), replace=False))
+        ref = oracle_mod.dgt(f, g, a, M, l1, l2, cols=cols)
+        assert rel(c[:, :, cols], ref) <= TOL[dtype], (L, a, M, l1, l2, plan.info)
+    assert len(branches) >= 2
+
+
 def test_full_size_covariances(torch_cuda, nsdgt):
     """SURVEY §4 T4 at config 5's full size on the fused path (no oracle): modulation by k
     channels rolls c along m; translation by x = a lambda2 j samples rolls c along n by
