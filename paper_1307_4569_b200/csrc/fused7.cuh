@@ -176,9 +176,10 @@ struct Args {
     int W, N, c, Kmod, beta;
     int S, lag, nA, nB;
     unsigned long long* log;   // dbg & 16: per-CTA phase timestamps (CTAs < 8, 4096 entries each)
-    int dbg;             // experiment knobs (0 in production; results are wrong with 1, 4, 8):
+    int dbg;             // experiment knobs (0 in production; results are wrong with all but 16):
                          // 1 no dependency spin, 4 no global stores, 8 no DFT arithmetic,
-                         // 16 phase trace (-DNSDGT_TRACE builds)
+                         // 16 phase trace (-DNSDGT_TRACE builds), 32 no G' loads,
+                         // 64 no c stores, 128 no ring stores
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
         const float4* G4 = A.Gp + ((int64_t)((j0 / AC) * 4 + h) * (R1 / 2)) * 128 + h8 * 8 + s8;
 #pragma unroll
         for (int kp = 8 * b; kp < 8 * b + 8 && kp < R1 / 2; ++kp) {
-            const float4 g = ldg_na(G4 + kp * 128);
+            const float4 g = (A.dbg & 32) ? make_float4(1.f, 0.f, 1.f, 0.f) : ldg_na(G4 + kp * 128);
             pre[2 * kp] = make_float2(g.x, g.y);
             pre[2 * kp + 1] = make_float2(g.z, g.w);
         }
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                                 }
                             },
                             [&](int r, const float2* y) {
-                                if (A.dbg & 4) return;
+                                if (A.dbg & (4 | 128)) return;
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) dst[(4 * r + (R1 / 4) * m2) * 16] = y[m2];
                             }, A.dbg, mark);
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                                 }
                             },
                             [&](int r, const float2* y) {
-                                if (A.dbg & 4) return;
+                                if (A.dbg & (4 | 64)) return;
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) {
                                     const int m = 16 * r + h8 + R1 * m2;
