@@ -6,9 +6,12 @@ Contract:
 One "step" = one pass of the whole hot path (Alg. 1: chirp/FFT front end, Zak/factorisation
 DGT, phase + remap) over this rank's shard of the config's batch, inputs resident in HBM.
 Default workload: BASELINE.json config 5 (L=262144, a=128, M=512, lambda=1/2, W=1024,
-complex64), the config BASELINE.json shards over 1/2/4/8 GPUs.  W is split contiguously
-over ranks (fixed total work => "scaling": "strong"); there is no data-path collective.
-Rank 0 prints ONE JSON line.  For N > 1 launch with torchrun (one process per GPU, NCCL).
+complex64).  Multi-GPU: the signals are independent units, so each rank transforms its own
+batch of W signals (signals [rank W, (rank + 1) W) of the seeded stream; "scaling": "weak",
+value = all ranks' coefficients / max-over-ranks time); --scaling strong splits one batch of
+W contiguously instead.  There is no data-path collective.  Rank 0 prints ONE JSON line.
+For N > 1 the driver launches torchrun (one process per GPU, NCCL); a plain
+``python bench.py --gpus N`` re-executes itself under torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
@@ -35,9 +38,26 @@ def dist_setup(n_gpus):
     return pd.init()
 
 
-def shard(W, ws, rank):
+def shard(W, ws, rank, scaling="weak"):
+    """This rank's signals [w0, w1): weak scaling -- every rank its own batch of W signals;
+    strong -- one batch of W split contiguously."""
     from paper_1307_4569_b200 import dist as pd
+    if scaling == "weak":
+        return rank * W, (rank + 1) * W
     return pd.shard(W, ws, rank)
+
+
+def spawn_ranks(n):
+    """Re-execute this script under torch.distributed.run with n ranks on 127.0.0.1 (used when
+    ``--gpus N > 1`` is given without a torchrun environment).  Returns the launcher's exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def barrier(ws):
@@ -134,6 +154,23 @@ def ncu_traffic(workload, kernel):
         return None
 
 
+def fp_peak(dtype):
+    """Measured CUDA-core FMA peak in TFLOP/s (2 flops per FMA) for the working precision:
+    profiles/r01_microbench.json (tools/microbench.cu on a B200 of this pool)."""
+    key = "fp32_ffma_reg_Tinstr_s" if dtype == "c64" else "fp64_dfma_reg_Tinstr_s"
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_microbench.json")) as fh:
+            return 2.0 * float(json.load(fh)[key]), f"measured ({key} x 2, profiles/r01_microbench.json)"
+    except Exception:  # noqa: BLE001
+        return (74.4 if dtype == "c64" else 37.2), "nominal (148 SMs x 128 FP32 / 64 FP64 lanes x 2 x 1.965 GHz)"
+
+
+def ncu_traffic_chain(workload, stats):
+    """Summed per-chunk DRAM bytes of a multi-kernel chain, if every kernel has a capture."""
+    vals = [ncu_traffic(workload, k["name"]) for k in stats]
+    return None if any(v is None for v in vals) else float(sum(vals))
+
+
 def oracle_sample(wl, budget_s, max_signals=None):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload.
     Returns (coefs/s, cores, description)."""
@@ -142,14 +179,15 @@ def oracle_sample(wl, budget_s, max_signals=None):
     import oracle
     from synthetic import batch, window
     g = window(wl)
-    cores = oracle.threads()
+    # all host cores, also under torchrun (which sets OMP_NUM_THREADS=1 for its ranks)
+    cores = len(os.sched_getaffinity(0))
     variant = "literal" if wl.L * wl.M <= 4096 * 64 else "regrouped"
     # probe: one signal on a column subset to size the sample
     ncol = min(wl.N, 64)
     cols = np.arange(ncol)
     f1 = batch(wl, 0, 1)
     t0 = time.perf_counter()
-    oracle.dgt(f1, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols, variant=variant)
+    oracle.dgt(f1, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols, variant=variant, nthreads=cores)
     tp = time.perf_counter() - t0
     per_col = max(tp / ncol, 1e-7)
     ncols_total = int(max(1, min(wl.N * (max_signals or wl.W), budget_s / per_col)))
@@ -158,7 +196,7 @@ def oracle_sample(wl, budget_s, max_signals=None):
     f = batch(wl, 0, nsig)
     cols = np.arange(cols_per_sig)
     t0 = time.perf_counter()
-    oracle.dgt(f, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols, variant=variant)
+    oracle.dgt(f, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols, variant=variant, nthreads=cores)
     dt = time.perf_counter() - t0
     coefs = nsig * wl.M * cols_per_sig
     desc = (f"oracle {'O1 literal' if variant == 'literal' else 'O2 regrouped'} sum (fp64, OpenMP), "
@@ -174,12 +212,12 @@ def oracle_sample_inverse(wl, budget_s):
     import oracle
     from synthetic import window
     g = window(wl)
-    cores = oracle.threads()
+    cores = len(os.sched_getaffinity(0))
     rng = np.random.default_rng(0)
     c = rng.standard_normal((1, wl.M, wl.N)) + 1j * rng.standard_normal((1, wl.M, wl.N))
     n, t0 = 0, time.perf_counter()
     while n == 0 or (time.perf_counter() - t0 < budget_s and n < wl.W):
-        oracle.idgt(c, g, wl.a, wl.M, wl.lam1, wl.lam2, variant="regrouped")
+        oracle.idgt(c, g, wl.a, wl.M, wl.lam1, wl.lam2, variant="regrouped", nthreads=cores)
         n += 1
     dt = time.perf_counter() - t0
     desc = f"oracle S2 regrouped synthesis (fp64, OpenMP), {n} whole signal(s) of {wl.name}"
@@ -205,7 +243,7 @@ def run_reference(args, wl, ws, rank):
     line = {
         "impl": "reference", "metric": METRIC_INV if args.inverse else METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, synthetic/workloads.py)",
         "config": {"workload": wl.name, "L": wl.L, "a": wl.a, "M": wl.M, "lambda": [wl.lam1, wl.lam2],
                    "W": wl.W, "parallelism": "host cores (OpenMP)"},
@@ -231,13 +269,32 @@ def main():
     ap.add_argument("--max-chunk", type=int, default=0)
     ap.add_argument("--inverse", action="store_true",
                     help="time the synthesis (dgt_execute_inverse, c -> f) instead of the forward DGT")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: W signals per rank (default); strong: W signals split over the ranks")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="bring up the ranks and print the shard plan only (no GPU work; tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
 
     from synthetic import config
     wl = config(args.config)
     ws, rank, local = dist_setup(args.gpus)
+    if args.dry_run:
+        import torch.distributed as dist
+        w0, w1 = shard(wl.W, ws, rank, args.scaling)
+        parts = [None] * ws
+        if ws > 1:
+            dist.all_gather_object(parts, (rank, w0, w1))
+            dist.destroy_process_group()
+        else:
+            parts = [(rank, w0, w1)]
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": ws, "requested_gpus": args.gpus, "scaling": args.scaling,
+                              "workload": wl.name, "shards": [list(p) for p in parts]}), flush=True)
+        return 0
 
     if args.impl == "reference":
         rc = run_reference(args, wl, ws, rank)
@@ -253,7 +310,7 @@ def main():
     from synthetic import batch, window
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    w0, w1 = shard(wl.W, ws, rank)
+    w0, w1 = shard(wl.W, ws, rank, args.scaling)
     Wr = w1 - w0
     g = window(wl)
     plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, real_input=wl.real_input,
@@ -313,25 +370,33 @@ def main():
     ms_total = e0.elapsed_time(e1) if flush is None else sum(a.elapsed_time(b) for a, b in pairs)
     ms_total_max = allreduce_max(ms_total, ws)
     ms_per_step = ms_total_max / args.steps
-    coefs_per_step = wl.W * wl.M * wl.N
-    value = coefs_per_step / (ms_per_step * 1e-3)
+    coefs_per_step = (w1 - w0) * wl.M * wl.N
+    coefs_all = allreduce_sum(coefs_per_step, ws)   # every rank's units (weak: ws x W signals)
+    value = coefs_all / (ms_per_step * 1e-3)
 
-    # roofline of the dominant kernel (largest summed duration): SURVEY 8(d)'s algorithmic bytes
-    # per signal (input + coefficients, window once) x the signals one launch of that kernel
-    # processes (a multi-kernel path -- config 4's cuFFT / zak_ct / out_f4096 -- runs each kernel
-    # once per chunk of signals; intermediates are not algorithmic)
+    # Roofline: SURVEY 8(d)'s algorithmic bytes per signal (input + coefficients, window once)
+    # over the time of the kernels that move them.  The fused path is one kernel per step; a
+    # multi-kernel path (config 4: cuFFT + zak_ct + out_f4096 per chunk of signals) is charged
+    # the summed time of its whole chain per chunk -- intermediates are not algorithmic bytes.
     dom = max(stats, key=lambda s: s["ms"])
-    launches_per_step = dom["launches"] / args.steps
+    chain_ms = sum(k["ms"] for k in stats)
+    launches_per_step = dom["launches"] / args.steps   # chunks per step (one launch of each kind per chunk)
     per_launch_bytes = step_bytes / launches_per_step
-    per_launch_ms = dom["ms"] / dom["launches"]
-    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    per_chunk_ms = chain_ms / dom["launches"]
+    achieved = per_launch_bytes / (per_chunk_ms * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
-    traffic = ncu_traffic(wl.name, dom["name"])
+    fpk, fpk_src = fp_peak(wl.dtype)
+    chain_flops = sum(k["flops"] for k in stats)
+    traffic = ncu_traffic(wl.name, dom["name"]) if len(stats) == 1 else ncu_traffic_chain(wl.name, stats)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": dom["name"], "peak_source": peak_src,
-                "kernel_ms_per_launch": per_launch_ms, "algorithmic_bytes_per_launch": per_launch_bytes,
-                "kernel_share_of_step": dom["ms"] / ms_total if ms_total > 0 else None,
-                "model_tflops": dom["flops"] / (dom["ms"] * 1e-3) / 1e12,
+                "traffic": traffic, "kernel": dom["name"] if len(stats) == 1 else "+".join(k["name"] for k in stats),
+                "peak_source": peak_src,
+                "kernel_ms_per_launch": per_chunk_ms, "algorithmic_bytes_per_launch": per_launch_bytes,
+                "dominant_kernel": dom["name"],
+                "kernel_share_of_step": chain_ms / ms_total if ms_total > 0 else None,
+                "model_tflops": chain_flops / (chain_ms * 1e-3) / 1e12,
+                "compute_peak_tflops": fpk, "compute_peak_source": fpk_src,
+                "compute_frac": chain_flops / (chain_ms * 1e-3) / 1e12 / fpk,
                 "kernels": stats}
     step_gbs = step_bytes / (ms_total / args.steps * 1e-3) / 1e9
 
@@ -352,7 +417,7 @@ def main():
         torch.cuda.synchronize()
         barrier(ws)
         e2e_ms = allreduce_max(ee0.elapsed_time(ee1), ws) / args.e2e_steps
-        e2e = {"value": coefs_per_step / (e2e_ms * 1e-3), "unit": UNIT,
+        e2e = {"value": coefs_all / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(allreduce_sum(f_host.numel() * f_host.element_size(), ws)),
                "d2h_bytes_per_step": int(allreduce_sum(c_host.numel() * c_host.element_size(), ws)),
                "ms_per_step": e2e_ms, "steps": args.e2e_steps,
@@ -374,11 +439,13 @@ def main():
         info = plan.info
         line = {
             "metric": METRIC_INV if args.inverse else METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded, synthetic/workloads.py)",
             "config": {"workload": wl.name, "L": wl.L, "a": wl.a, "M": wl.M, "N": wl.N,
-                       "lambda": [wl.lam1, wl.lam2], "W": wl.W, "global_batch": wl.W,
-                       "parallelism": f"dp{ws} (signals sharded, no collective on the data path)",
+                       "lambda": [wl.lam1, wl.lam2], "W": wl.W,
+                       "global_batch": wl.W * ws if args.scaling == "weak" else wl.W,
+                       "signals_per_rank": w1 - w0,
+                       "parallelism": f"dp{ws} (independent signals per rank, no collective on the data path)",
                        "branch": nsdgt.BRANCH_NAMES[info["branch"]], "shear": [info["s0"], info["s1"]],
                        "inner": {"a": info["ia"], "M": info["iM"], "c": info["c"], "d": info["d"],
                                  "p": info["p"], "q": info["q"]},

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -1216,6 +1217,7 @@ __global__ void k_ola_add(cx<T>* c, const cx<T>* cb, int64_t M, int64_t N, int64
 
 struct Plan;
 static void free_plan(Plan* P);
+static constexpr int64_t kMaxChunk = 8192;   // signals per launch pair of the generic path
 struct Plan {
     dgt_lattice_info info{};
     int dtype = DGT_C64;
@@ -1254,12 +1256,13 @@ struct Plan {
     int gA = 0, gB = 0;      // Zak / output kernels with per-CTA buffers in global scratch
     unsigned char* scrA = nullptr;
     unsigned char* scrB = nullptr;
-    // synthesis (dgt_execute_inverse): chunk, zak_adj_kernel smem, workspace (allocated on
-    // first use: C intermediate + F-branch spectra)
+    // synthesis (dgt_execute_inverse): chunk, zak_adj_kernel smem, workspace (made at plan
+    // time by alloc_workspace: C intermediate + F-branch spectra, shared with the forward's)
     int64_t inv_chunk = 1;
     size_t smemAinv = 0;
     void* Cinv = nullptr;
     void* finv = nullptr;
+    int inv_alias = 0;       // bit 0: Cinv is Cws, bit 1: finv is fhat (not freed twice)
     int zct = 0;             // zak_kernel compile-time inner length (0 = runtime radices)
     int inv_generic = 0;     // experiment knob (NSDGT_INV_GENERIC, read at plan time): generic synthesis
     int outct = 0;           // out_kernel compile-time inner channel count (0 = runtime radices)
@@ -1324,6 +1327,8 @@ static void free_plan(Plan* P) {
     if (P->ola) free_plan(P->ola);
     if (P->ola_x) cudaFree(P->ola_x);
     if (P->ola_c) cudaFree(P->ola_c);
+    if (P->inv_alias & 1) P->Cinv = nullptr;
+    if (P->inv_alias & 2) P->finv = nullptr;
     void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
                     P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv, P->gt64,
                     P->scrA, P->scrB};
@@ -1621,9 +1626,13 @@ static int configure(Plan* P, int64_t max_chunk) {
     if (P->zct) {
         // the constant-memory twiddles of fft_ct (same values for every plan; long-double
         // cos/sin of exact residues on the host, rounded once)
-        static std::once_flag once;
-        static int tw_rc = 0;
-        std::call_once(once, [] {
+        // __constant__ memory is per device: upload once per device (mutex-guarded set of
+        // devices done; a failed upload is retried by the next plan instead of poisoning it)
+        static std::mutex tw_mu;
+        static std::set<int> tw_done;
+        int tw_rc = 0;
+        {
+            std::lock_guard<std::mutex> lk(tw_mu);
             auto fill = [](auto& dsym, auto& fsym, int n) {
                 std::vector<double2> d(n);
                 std::vector<float2> f(n);
@@ -1635,8 +1644,13 @@ static int configure(Plan* P, int64_t max_chunk) {
                 return cudaMemcpyToSymbol(dsym, d.data(), sizeof(double2) * n) == cudaSuccess &&
                        cudaMemcpyToSymbol(fsym, f.data(), sizeof(float2) * n) == cudaSuccess;
             };
-            if (!fill(c_tw180d, c_tw180f, 180) || !fill(c_tw720d, c_tw720f, 720)) tw_rc = 1;
-        });
+            int dev = -1;
+            cudaGetDevice(&dev);
+            if (!tw_done.count(dev)) {
+                if (!fill(c_tw180d, c_tw180f, 180) || !fill(c_tw720d, c_tw720f, 720)) tw_rc = 1;
+                else tw_done.insert(dev);
+            }
+        }
         if (tw_rc) return fail(DGT_ECUDA, "constant twiddle upload");
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
@@ -1679,6 +1693,11 @@ static int configure(Plan* P, int64_t max_chunk) {
     const size_t per_sig = (size_t)I.iM * I.iN * e;
     int64_t ch = std::max<int64_t>(1, (int64_t)((size_t)(l2 > 0 ? l2 : (64 << 20)) * 2 / 5 / per_sig));
     if (!std::getenv("NSDGT_CHUNK_L2")) ch = std::max<int64_t>(ch, (int64_t)((1ull << 30) / per_sig));
+    // the chunk is gridDim.y of the zak / out kernels and their adjoints (<= 65535); 8192
+    // signals of any lattice fill the GPU many times over, so tiny signals do not size a
+    // ~1 GiB workspace and cuFFT batches of 10^5 at plan time
+    ch = std::min<int64_t>(ch, kMaxChunk);
+    if (max_chunk > 65535) return fail(DGT_EINVAL, "max_chunk > 65535 (grid y limit of the chunk kernels)");
     P->inv_chunk = max_chunk > 0 ? max_chunk : ch;
     if (max_chunk > 0) ch = max_chunk;
     P->chunk = ch;
@@ -1717,6 +1736,28 @@ static int alloc_workspace(Plan* P, int64_t Wc) {
             cufftHandle h;
             int rc = get_fft_plan(P, b, nullptr, &h);
             if (rc) return rc;
+        }
+    }
+    // synthesis workspace (dgt_execute_inverse), also made here so that no execute entry point
+    // allocates: the forward chunk intermediate and spectra serve it when they have its size
+    // (one plan never runs two executes at once -- include/nsdgt.h), else its own buffers
+    if (!P->fast || P->inv_generic) {
+        const size_t inv_need = (size_t)P->inv_chunk * I.iM * I.iN * P->esz;
+        if (!P->fast && P->inv_chunk <= Wc) {
+            P->Cinv = P->Cws;
+            P->inv_alias |= 1;
+        } else {
+            CUDA_TRY(cudaMalloc(&P->Cinv, inv_need));
+            P->ws_bytes += inv_need;
+        }
+        if (I.branch == DGT_BRANCH_FREQ) {
+            if (P->fhat && P->ib <= P->fb) {
+                P->finv = P->fhat;
+                P->inv_alias |= 2;
+            } else {
+                CUDA_TRY(cudaMalloc(&P->finv, (size_t)P->ib * I.L * P->esz));
+                P->ws_bytes += (size_t)P->ib * I.L * P->esz;
+            }
         }
     }
     return DGT_OK;
@@ -1802,10 +1843,7 @@ static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStrea
     // frequency shear: spectra of a batch of ib signals (a multiple of the chunk, ~192 MB) are
     // collected and inverse-transformed by one batched cuFFT call
     const int64_t ib = freq ? P->ib : W;
-    if (!P->Cinv) {
-        CUDA_TRY(cudaMalloc(&P->Cinv, (size_t)P->inv_chunk * I.iM * I.iN * P->esz));
-        if (freq) CUDA_TRY(cudaMalloc(&P->finv, (size_t)ib * I.L * P->esz));
-    }
+    if (!P->Cinv || (freq && !P->finv)) return fail(DGT_EINVAL, "synthesis workspace missing (made at plan time)");
     for (int64_t b0 = 0; b0 < W; b0 += ib) {
         const int64_t nb = std::min<int64_t>(ib, W - b0);
         for (int64_t w0 = b0; w0 < b0 + nb; w0 += P->inv_chunk) {
@@ -1928,6 +1966,8 @@ int dgt_lattice_plan(int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, in
     return DGT_OK;
 }
 
+static int alloc_host_staging(Plan* P);
+
 int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int dtype,
              int flags, int64_t max_chunk, int force_shear, int64_t s0, int64_t s1, void* cuda_stream) {
     if (!out || !g) return fail(DGT_EINVAL, "null pointer");
@@ -1956,6 +1996,7 @@ int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64
         P->chunk = max_chunk > 0 ? max_chunk : fast_chunk(&P->fp);
     }
     if (!rc) rc = alloc_workspace(P, P->chunk);
+    if (!rc) rc = alloc_host_staging(P);
     if (rc) {
         free_plan(P);
         return rc;
@@ -2149,68 +2190,84 @@ int dgt_window_dual(dgt_plan_t plan, int kind, void* out, int flags, void* cuda_
     return rc;
 }
 
+// Host-buffer staging of dgt_execute_host, made at plan time: two copy streams, events and two
+// slots of sw signals (~64 MB of output per slot, at most kMaxChunk signals, a multiple of the
+// compute chunk when that is smaller; flat from 32 to 512 MB per slot on config 5: the two copy
+// directions overlap each other and the kernels at the PCIe floor).
+static int alloc_host_staging(Plan* P) {
+    const dgt_lattice_info& I = P->info;
+    const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
+    const size_t per_f = (size_t)I.L * ein, per_c = (size_t)I.M * I.N * P->esz;
+    int64_t sw = std::max<int64_t>(1, std::min<int64_t>(kMaxChunk, (int64_t)((64ull << 20) / per_c)));
+    if (P->chunk < sw) sw = sw / P->chunk * P->chunk;
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        CUDA_TRY(cudaEventCreateWithFlags(&P->ev_in[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&P->ev_comp[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&P->ev_out[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaMalloc(&P->stage_f[i], per_f * sw));
+        CUDA_TRY(cudaMalloc(&P->stage_c[i], per_c * sw));
+    }
+    P->stage_W = sw;
+    P->ws_bytes += 2 * (per_f + per_c) * sw;
+    return DGT_OK;
+}
+
 int dgt_execute_host(dgt_plan_t plan, const void* f_host, void* c_host, int64_t W, void* cuda_stream) {
     Plan* P = (Plan*)plan;
     if (!P) return fail(DGT_EINVAL, "null plan");
     if (W < 0) return fail(DGT_EINVAL, "W < 0");
     if (W == 0) return DGT_OK;
     if (!f_host || !c_host) return fail(DGT_EINVAL, "null pointer");
+    if (!P->s_in || P->stage_W < 1) return fail(DGT_EINVAL, "host staging missing (made at plan time)");
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const dgt_lattice_info& I = P->info;
     const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
     const size_t per_f = (size_t)I.L * ein, per_c = (size_t)I.M * I.N * P->esz;
-    // staging chunk: ~128 MB of output per slot (flat from 32 to 512 MB on cfg5: the two
-    // copy directions overlap each other and the kernels at the PCIe floor)
-    int64_t sw = std::max<int64_t>(1, (int64_t)((128ull << 20) / per_c));
-    // a multiple of the compute chunk when that is smaller (the fused path has no chunk
-    // limit: P->chunk is then huge and the staging size alone decides)
-    if (P->chunk < sw) sw = sw / P->chunk * P->chunk;
-    sw = std::min<int64_t>(sw, W);
-    if (!P->s_in) {
-        CUDA_TRY(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
-        CUDA_TRY(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
-        for (int i = 0; i < 2; ++i) {
-            CUDA_TRY(cudaEventCreateWithFlags(&P->ev_in[i], cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&P->ev_comp[i], cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&P->ev_out[i], cudaEventDisableTiming));
+    const int64_t sw = std::min<int64_t>(P->stage_W, W);
+    // Once a copy is enqueued, every return waits for the three streams first: the caller may
+    // free or reuse its host buffers as soon as this returns, even on an error.
+    bool started = false;
+    auto drain = [&](int rc) {
+        if (started) {
+            cudaStreamSynchronize(P->s_in);
+            cudaStreamSynchronize(P->s_out);
+            cudaStreamSynchronize(st);
         }
-    }
-    if (P->stage_W < sw) {
-        for (int i = 0; i < 2; ++i) {
-            if (P->stage_f[i]) cudaFree(P->stage_f[i]);
-            if (P->stage_c[i]) cudaFree(P->stage_c[i]);
-            P->stage_f[i] = P->stage_c[i] = nullptr;
-        }
-        P->stage_W = 0;
-        for (int i = 0; i < 2; ++i) {
-            CUDA_TRY(cudaMalloc(&P->stage_f[i], per_f * sw));
-            CUDA_TRY(cudaMalloc(&P->stage_c[i], per_c * sw));
-        }
-        P->stage_W = sw;
-    }
+        return rc;
+    };
+#define HOST_TRY(x)                                                                  \
+    do {                                                                             \
+        cudaError_t e_ = (x);                                                        \
+        if (e_ != cudaSuccess) return drain(fail(DGT_ECUDA, cudaGetErrorString(e_))); \
+    } while (0)
     // the caller's stream must be ordered before our copies start
-    CUDA_TRY(cudaEventRecord(P->ev_out[0], st));
-    CUDA_TRY(cudaStreamWaitEvent(P->s_in, P->ev_out[0], 0));
-    CUDA_TRY(cudaEventRecord(P->ev_out[1], st));
+    HOST_TRY(cudaEventRecord(P->ev_out[0], st));
+    HOST_TRY(cudaStreamWaitEvent(P->s_in, P->ev_out[0], 0));
+    HOST_TRY(cudaEventRecord(P->ev_out[1], st));
     int64_t i = 0;
     for (int64_t w0 = 0; w0 < W; w0 += sw, ++i) {
         const int slot = (int)(i & 1);
         const int64_t wc = std::min<int64_t>(sw, W - w0);
-        CUDA_TRY(cudaStreamWaitEvent(P->s_in, P->ev_out[slot], 0));
-        CUDA_TRY(cudaMemcpyAsync(P->stage_f[slot], (const char*)f_host + w0 * per_f, wc * per_f,
+        HOST_TRY(cudaStreamWaitEvent(P->s_in, P->ev_out[slot], 0));
+        started = true;
+        HOST_TRY(cudaMemcpyAsync(P->stage_f[slot], (const char*)f_host + w0 * per_f, wc * per_f,
                                  cudaMemcpyHostToDevice, P->s_in));
-        CUDA_TRY(cudaEventRecord(P->ev_in[slot], P->s_in));
-        CUDA_TRY(cudaStreamWaitEvent(st, P->ev_in[slot], 0));
+        HOST_TRY(cudaEventRecord(P->ev_in[slot], P->s_in));
+        HOST_TRY(cudaStreamWaitEvent(st, P->ev_in[slot], 0));
         int rc = execute(P, P->stage_f[slot], P->stage_c[slot], wc, st);
-        if (rc) return rc;
-        CUDA_TRY(cudaEventRecord(P->ev_comp[slot], st));
-        CUDA_TRY(cudaStreamWaitEvent(P->s_out, P->ev_comp[slot], 0));
-        CUDA_TRY(cudaMemcpyAsync((char*)c_host + w0 * per_c, P->stage_c[slot], wc * per_c, cudaMemcpyDeviceToHost,
+        if (rc) return drain(rc);
+        HOST_TRY(cudaEventRecord(P->ev_comp[slot], st));
+        HOST_TRY(cudaStreamWaitEvent(P->s_out, P->ev_comp[slot], 0));
+        HOST_TRY(cudaMemcpyAsync((char*)c_host + w0 * per_c, P->stage_c[slot], wc * per_c, cudaMemcpyDeviceToHost,
                                  P->s_out));
-        CUDA_TRY(cudaEventRecord(P->ev_out[slot], P->s_out));
+        HOST_TRY(cudaEventRecord(P->ev_out[slot], P->s_out));
     }
-    CUDA_TRY(cudaStreamSynchronize(P->s_out));
-    CUDA_TRY(cudaStreamSynchronize(st));
+#undef HOST_TRY
+    const cudaError_t e1 = cudaStreamSynchronize(P->s_out), e2 = cudaStreamSynchronize(st);
+    cudaStreamSynchronize(P->s_in);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(DGT_ECUDA, cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
     return DGT_OK;
 }
 

@@ -14,10 +14,13 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/nsdgt.h"
 #include "cplx.cuh"
 #include "fused7.cuh"
 #include "fused7_adj.cuh"
+#include "fused8.cuh"
 
 namespace nsdgt {
 
@@ -25,7 +28,9 @@ template <typename T>
 __global__ void k_window_factor(cx<T>* G, const double2* gt, int64_t L, int64_t c, int64_t d, int64_t p, int64_t q);
 
 struct FastPlan {
-    int kind = 0;  // 0 = none (generic path); 2 = fused7
+    int kind = 0;  // 0 = none (generic path); 2 = fused persistent kernel (fused8, or fused7)
+    int xdb = 0;   // fused7t: double-buffered exchange (NSDGT_XDB=1)
+    int ver = 7;   // forward kernel: 7 = fused7 (default), 9 = fused7t (TMA tile loads), 8 = fused8 (NSDGT_FUSED)
     const char* name = "none";
     int D = 0, MM = 0, Q = 0, c = 0, N = 0;
     int64_t L = 0;
@@ -55,6 +60,40 @@ static void launch7(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
 template <int D, int MINB>
 static void launch7r(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
     v7::fused7_kernel<D, MINB, (MINB <= 3), true><<<grid, v7::Cfg<D>::NT, smem, st>>>(a);
+}
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+// 2-D map over a row-major array of 8-byte elements: cols x rows, row pitch in bytes, boxes of
+// box_cols x box_rows
+static bool encode_map_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
+                          uint32_t box_cols, uint32_t box_rows) {
+    auto fn = tensor_map_encoder();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {pitch};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <int D, int MINB, bool XDB = false>
+static void launch7t(const v7::Args& a, const v7::Maps& m, int grid, size_t smem, cudaStream_t st) {
+    v7::fused7t_kernel<D, MINB, XDB><<<grid, v7::Cfg<D>::NT, smem, st>>>(a, m);
+}
+template <int D, int MINB, bool REAL = false>
+static void launch8(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
+    v8::fused8_kernel<D, MINB, REAL><<<grid, v8::Cfg<D>::NT, smem, st>>>(a);
 }
 template <int D, int MINB>
 static void launch7a(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
@@ -97,24 +136,44 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     // kernel variant: CTAs per SM, measured best 3 for D = 512 (more CTAs leave too little L1
     // next to 3 x 53 KB of shared memory: the ring stores use it), 5 for D = 256 (36 KB, 91
     // registers).  NSDGT_CTAS overrides (experiments).
-    int minb = D == 512 ? 3 : 5;
-    if (const char* e = std::getenv("NSDGT_CTAS")) minb = std::max(3, std::min(D == 512 ? 4 : 5, std::atoi(e)));
+    fp->ver = 7;
+    if (const char* e = std::getenv("NSDGT_FUSED")) {
+        const int v = std::atoi(e);
+        fp->ver = (v == 7 || v == 9) ? v : 8;
+    }
+    const bool v8k = fp->ver == 8;
+    fp->xdb = (fp->ver == 9 && std::getenv("NSDGT_XDB") && std::atoi(std::getenv("NSDGT_XDB"))) ? 1 : 0;
+    int minb = v8k ? 2 : D == 512 ? 3 : 5;
+    if (const char* e = std::getenv("NSDGT_CTAS"))
+        minb = v8k ? std::max(2, std::min(D == 512 ? 2 : 3, std::atoi(e))) : std::max(3, std::min(D == 512 ? 4 : 5, std::atoi(e)));
     {
         const void* ka = D == 512 ? (const void*)v7::fused7a_kernel<512, 3> : (const void*)v7::fused7a_kernel<256, 5>;
         const size_t sm = D == 512 ? v7::Cfg<512>::SMEM : v7::Cfg<256>::SMEM;
         if (cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return DGT_ECUDA;
         fp->smem_adj = sm;
     }
-    const void* kfn = D == 512 ? (minb == 4 ? (const void*)v7::fused7_kernel<512, 4> : (const void*)v7::fused7_kernel<512, 3>)
-                               : (minb == 5   ? (const void*)v7::fused7_kernel<256, 5>
-                                  : minb == 4 ? (const void*)v7::fused7_kernel<256, 4>
-                                              : (const void*)v7::fused7_kernel<256, 3>);
-    const size_t smem = D == 512 ? v7::Cfg<512>::SMEM : v7::Cfg<256>::SMEM;
+    const void* kfn = v8k ? (D == 512   ? (const void*)v8::fused8_kernel<512, 2>
+                             : minb == 3 ? (const void*)v8::fused8_kernel<256, 3>
+                                         : (const void*)v8::fused8_kernel<256, 2>)
+                      : fp->ver == 9 && fp->xdb ? (D == 512 ? (const void*)v7::fused7t_kernel<512, 3, true>
+                                                            : (const void*)v7::fused7t_kernel<256, 4, true>)
+                      : fp->ver == 9 ? (D == 512 ? (minb == 4 ? (const void*)v7::fused7t_kernel<512, 4>
+                                                              : (const void*)v7::fused7t_kernel<512, 3>)
+                                                 : (minb == 5 ? (const void*)v7::fused7t_kernel<256, 5>
+                                                              : (const void*)v7::fused7t_kernel<256, 4>))
+                      : D == 512 ? (minb == 4 ? (const void*)v7::fused7_kernel<512, 4> : (const void*)v7::fused7_kernel<512, 3>)
+                                 : (minb == 5   ? (const void*)v7::fused7_kernel<256, 5>
+                                    : minb == 4 ? (const void*)v7::fused7_kernel<256, 4>
+                                                : (const void*)v7::fused7_kernel<256, 3>);
+    const size_t smem = v8k ? (D == 512 ? v8::Cfg<512>::SMEM : v8::Cfg<256>::SMEM)
+                            : (D == 512 ? v7::Cfg<512>::SMEM + (fp->xdb ? v7::Cfg<512>::XE * 8 : 0)
+                                        : v7::Cfg<256>::SMEM + (fp->xdb ? v7::Cfg<256>::XE * 8 : 0));
+    const int nthreads = v8k ? v8::Cfg<512>::NT : v7::Cfg<512>::NT;
     if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return DGT_ECUDA;
     int per_sm = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, v7::Cfg<512>::NT, smem) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthreads, smem) != cudaSuccess || per_sm < 1)
         return DGT_OK;   // cannot host the persistent kernel: generic path
     // persistent kernel: every CTA must be resident (the occupancy query bounds the grid)
     if (const char* e = std::getenv("NSDGT_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
@@ -126,7 +185,8 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     ga.Gp = (float4*)fp->Gp; ga.G64 = G64; ga.L = L; ga.K = K;
     ga.M = (int)M; ga.D = (int)D; ga.Q = (int)Q; ga.c = (int)I.c; ga.beta = (int)beta; ga.R1 = (int)(D / 16);
     ga.layout = 0;
-    v7::k_gprime<<<(unsigned)std::min<int64_t>((M * Q * D + 255) / 256, 148 * 64), 256, 0, st>>>(ga);
+    if (v8k) v8::k_gprime8<<<(unsigned)std::min<int64_t>((M * Q * D + 255) / 256, 148 * 64), 256, 0, st>>>(ga);
+    else v7::k_gprime<<<(unsigned)std::min<int64_t>((M * Q * D + 255) / 256, 148 * 64), 256, 0, st>>>(ga);
     // the same table in the synthesis kernel's order
     if (cudaMalloc(&fp->Gpa, sizeof(float2) * (size_t)M * Q * D) != cudaSuccess) { cudaFree(G64); return DGT_ENOMEM; }
     ga.Gp = (float4*)fp->Gpa;
@@ -139,7 +199,7 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     fp->grid = per_sm * sms;
     fp->smem = smem;
     fp->D = (int)D; fp->MM = (int)M; fp->Q = (int)Q; fp->c = (int)I.c; fp->N = (int)N; fp->L = L;
-    fp->nA = (int)(M / v7::Cfg<512>::ACOL);
+    fp->nA = (int)(M / (v8k ? v8::Cfg<512>::ACOL : v7::Cfg<512>::ACOL));
     fp->nB = (int)(N / 16);
     fp->Kmod = (int)(K % D);
     fp->beta = (int)beta;
@@ -159,7 +219,7 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     if (const char* e = std::getenv("NSDGT_LAG")) fp->lag = std::max(0, std::atoi(e));
     if (fp->lag >= fp->S) fp->lag = fp->S - 1;
     if (std::getenv("NSDGT_VERBOSE"))
-        std::fprintf(stderr, "fused7: D=%d CTAs/SM=%d grid=%d smem/CTA=%zu B ring S=%d lag=%d\n", (int)D, per_sm,
+        std::fprintf(stderr, "fused%d: D=%d CTAs/SM=%d grid=%d smem/CTA=%zu B ring S=%d lag=%d\n", fp->ver, (int)D, per_sm,
                      fp->grid, smem, fp->S, fp->lag);
     // job queue + per-slot completion counters (allocated here: execute allocates nothing)
     if (cudaMalloc(&fp->counters, sizeof(int) * (1 + 2 * fp->S)) != cudaSuccess) return DGT_ENOMEM;
@@ -176,14 +236,16 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, ka, v7::Cfg<512>::NT, fp->smem_adj) != cudaSuccess ||
             per_sm_a < 1)
             return DGT_ECUDA;
-        fp->grid_adj = std::min(per_sm * sms, per_sm_a * sms);
+        fp->grid_adj = v8k ? per_sm_a * sms : std::min(per_sm * sms, per_sm_a * sms);
     }
     {   // real-input variant (default occupancy): attribute + resident grid
-        const void* kr = D == 512 ? (const void*)v7::fused7_kernel<512, 3, true, true>
-                                  : (const void*)v7::fused7_kernel<256, 5, false, true>;
+        const void* kr = v8k ? (D == 512 ? (const void*)v8::fused8_kernel<512, 2, true>
+                                         : (const void*)v8::fused8_kernel<256, 2, true>)
+                             : D == 512 ? (const void*)v7::fused7_kernel<512, 3, true, true>
+                                        : (const void*)v7::fused7_kernel<256, 5, false, true>;
         int per_sm_r = 0;
         if (cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_r, kr, v7::Cfg<512>::NT, smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_r, kr, nthreads, smem) != cudaSuccess ||
             per_sm_r < 1)
             return DGT_ECUDA;
         fp->grid_real = std::min(per_sm * sms, per_sm_r * sms);
@@ -195,7 +257,7 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     fp->E = E;
     fp->esz = sizeof(float2);
     fp->kind = 2;
-    fp->name = "fused7_t_p1";
+    fp->name = v8k ? "fused8_t_p1" : fp->ver == 9 ? "fused7t_t_p1" : "fused7_t_p1";
     return DGT_OK;
 }
 
@@ -236,7 +298,25 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
         cudaMemsetAsync(fp->tracelog, 0, sizeof(unsigned long long) * 8 * 4096, st);
         a.log = fp->tracelog;
     }
-    if (real_in) {   // the real variants are compiled for the default occupancy only
+    if (fp->ver == 9 && !real_in) {
+        v7::Maps m;
+        const int64_t D = fp->D, M = fp->MM, Q = fp->Q;
+        if (!encode_map_2d(&m.f, f, (uint64_t)M, (uint64_t)(W * D), (uint64_t)M * 8, 8, 256) ||
+            !encode_map_2d(&m.ws, ws, (uint64_t)(Q * D), (uint64_t)fp->S * M, (uint64_t)Q * D * 8, 8, 256))
+            return DGT_ECUDA;
+        if (fp->xdb) (fp->D == 512 ? launch7t<512, 3, true> : launch7t<256, 4, true>)(a, m, fp->grid, fp->smem, st);
+        else if (fp->D == 512) (fp->minb == 4 ? launch7t<512, 4> : launch7t<512, 3>)(a, m, fp->grid, fp->smem, st);
+        else (fp->minb == 5 ? launch7t<256, 5> : launch7t<256, 4>)(a, m, fp->grid, fp->smem, st);
+    } else if (fp->ver == 8) {
+        if (real_in) {
+            if (fp->D == 512) launch8<512, 2, true>(a, fp->grid_real, fp->smem, st);
+            else launch8<256, 2, true>(a, fp->grid_real, fp->smem, st);
+        } else if (fp->D == 512) {
+            launch8<512, 2>(a, fp->grid, fp->smem, st);
+        } else {
+            (fp->minb == 3 ? launch8<256, 3> : launch8<256, 2>)(a, fp->grid, fp->smem, st);
+        }
+    } else if (real_in) {   // the real variants are compiled for the default occupancy only
         if (fp->D == 512) launch7r<512, 3>(a, fp->grid_real, fp->smem, st);
         else launch7r<256, 5>(a, fp->grid_real, fp->smem, st);
     } else if (fp->D == 512) {

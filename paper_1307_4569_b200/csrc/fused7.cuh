@@ -39,9 +39,18 @@
 #include <cstdint>
 
 #include "cplx.cuh"
+#include "tma.cuh"
 
 namespace nsdgt {
 namespace v7 {
+
+// TMA descriptors of the fused kernels' bulk input tiles (TMA variant): f as a 2-D array
+// [W D rows][M columns] and the ring as [S M rows][Q D columns], 8-byte elements, boxes of
+// 8 columns x 256 rows (64-byte rows of a 32 KB tile, two boxes per tile)
+struct Maps {
+    CUtensorMap f;
+    CUtensorMap ws;
+};
 
 // ------------------------------------------------------------------------------------
 // packed FP32x2 complex arithmetic
@@ -272,9 +281,13 @@ __device__ __forceinline__ int xslot(int s) { return (((s & 1) << 2) | (s >> 1))
 // 16 values, barrier, read one sequence, barrier (the buffer holds one round).  before_sync
 // runs after this thread's first-round writes, after_sync right after the first barrier
 // (v is dead then unless NR = 2 -- the second-round values live in v[16..31]).
-template <int D, class Before, class After, class Emit, class Mark>
+struct NoMid {
+    __device__ void operator()() const {}
+};
+template <int D, class Before, class After, class Emit, class Mark, class Mid = NoMid>
 __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2, int s1, int t, int os, int oi,
-                                         Before&& before_sync, After&& after_sync, Emit&& emit, int dbg, Mark&& mark) {
+                                         Before&& before_sync, After&& after_sync, Emit&& emit, int dbg, Mark&& mark,
+                                         Mid&& mid = Mid()) {
     constexpr int R1 = Cfg<D>::R1, NR = Cfg<D>::NR;
     mark(10);
     if (!(dbg & 8)) dftR<R1>(v);
@@ -296,6 +309,7 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
         if (r == 0) before_sync();
         mark(12);
         __syncthreads();
+        if (r == 0) mid();   // every thread's stage-1 inputs of this tile have been consumed
         mark(13);
         float2 y[16];
 #pragma unroll
@@ -306,6 +320,44 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
         emit(r, y);
     }
     mark(14);
+}
+
+// The same tile with the exchange double-buffered: round k of the kernel (counted across
+// tiles by xb, uniform over the CTA) uses buffer k mod 2.  A buffer's previous readers (two
+// rounds back) finished before the barrier of the round in between, so a tile needs one
+// barrier per round and none at tile boundaries.
+template <int D, class Before, class After, class Emit, class Mid>
+__device__ __forceinline__ void dft_tile_db(float2* v, const float2* tw, float2* X2, int& xb, int s1, int t, int os,
+                                            int oi, Before&& before_sync, After&& after_sync, Emit&& emit, int dbg,
+                                            Mid&& mid) {
+    constexpr int R1 = Cfg<D>::R1, NR = Cfg<D>::NR;
+    if (!(dbg & 8)) dftR<R1>(v);
+    const float4* tw4 = reinterpret_cast<const float4*>(tw);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        float2* XB = X2 + xb * Cfg<D>::XR;
+        xb ^= 1;
+        float2* xw = XB + xslot(s1) + t;
+        const float2* xr = XB + xslot(os) + 17 * oi;
+#pragma unroll
+        for (int m = 0; m < 16; m += 2) {
+            const float4 w2 = lds128_nohoist(tw4 + ((16 * r + m) >> 1));
+            const float2 a = (r || m) ? cmw(v[16 * r + m], make_float2(w2.x, w2.y)) : v[16 * r];
+            const float2 b = cmw(v[16 * r + m + 1], make_float2(w2.z, w2.w));
+            xw[17 * m] = a;
+            xw[17 * (m + 1)] = b;
+            if ((m & 7) == 6) asm volatile("" ::: "memory");
+        }
+        if (r == 0) before_sync();
+        __syncthreads();
+        if (r == 0) mid();
+        float2 y[16];
+#pragma unroll
+        for (int tt = 0; tt < 16; ++tt) y[tt] = xr[tt];
+        if (r == NR - 1) after_sync();
+        if (!(dbg & 8)) dft16(y);
+        emit(r, y);
+    }
 }
 
 // FULLPF: the whole next tile's inputs are prefetched behind the current tile's stage 2
@@ -579,6 +631,237 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
         }
     }
     __syncthreads();   // the last job's stores are ordered before its completion signal
+    if (tid == 0) flush();
+}
+
+// ------------------------------------------------------------------------------------
+// fused7t: fused7 with the bulk input tiles (the Zak tile's f and the B tiles' ring lines,
+// 32 KB each) brought into shared memory by the TMA engine instead of per-thread loads.
+// The destination is the F buffer, which is idle exactly when those tiles are needed: an A
+// job's f tile lands there and is overwritten by F after the Zak stage 1; a B job never uses
+// F.  Thread 0 issues the copy of the next tile as soon as the current one's stage-1 inputs
+// are consumed (the first exchange barrier) -- for the next job in the last tile, when it is
+// ready -- so the tile loads need no registers and no L1 capacity, and arrive by an mbarrier
+// (transaction bytes).  Everything else (G' register prefetch, exchange, ring, c stores,
+// queue, counters) is fused7's.
+// ------------------------------------------------------------------------------------
+template <int D, int MINB, bool XDB = false, bool FULLPF = (MINB <= 3)>
+__global__ void __launch_bounds__(128, MINB) fused7t_kernel(Args A, const __grid_constant__ Maps tm) {
+    using K = Cfg<D>;
+    constexpr int R1 = K::R1, Q = K::Q, M = D, AC = K::ACOL, BT = K::BT;
+    constexpr int N = Q * D;
+    constexpr uint32_t TILE_BYTES = (uint32_t)D * 8 * 8;   // 8 columns x D rows x 8 bytes
+    static_assert(K::FE * 8 >= (int)TILE_BYTES, "F buffer holds one input tile");
+    static_assert((K::XE * 8) % 128 == 0, "TMA destination alignment");
+    extern __shared__ __align__(128) unsigned char smem_tma[];
+    float2* X2 = reinterpret_cast<float2*>(smem_tma);
+    float2* F = X2 + K::XE * (XDB ? 2 : 1);
+    float2* twt = F + K::FE;
+    __shared__ int jobsm[2];
+    __shared__ int jobdec[4];
+    __shared__ __align__(8) uint64_t mbar;
+    const int tid = threadIdx.x;
+    const int s8 = tid & 7, h8 = tid >> 3;
+    for (int e = tid; e < 16 * R1; e += K::NT) {
+        const int tt = e / R1, m = e % R1;
+        double sn, cs;
+        sincospi(-2.0 * (double)((tt * m) % D) / (double)D, &sn, &cs);
+        twt[tt * K::TWS + m] = make_float2((float)cs, (float)sn);
+    }
+    const float2* tw = twt + h8 * K::TWS;
+    auto mark = [](int) {};
+    int xb = 0;   // XDB: exchange buffer of the next round
+    // one tile: fused7's dft_tile, or the double-buffered one
+    auto tile = [&](float2* v, int os, int oi, auto&& before, auto&& after, auto&& emit, auto&& mid) {
+        if constexpr (XDB)
+            dft_tile_db<D>(v, tw, X2, xb, s8, h8, os, oi, before, after, emit, A.dbg, mid);
+        else
+            dft_tile<D>(v, tw, X2, s8, h8, os, oi, before, after, emit, A.dbg, mark, mid);
+    };
+    int* queue = A.ctr;
+    int* doneA = A.ctr + 1;
+    int* doneB = A.ctr + 1 + A.S;
+    const int64_t MQD = (int64_t)M * Q * D;
+    if (tid == 0) {
+        if (tma::saddr(F) & 127) __trap();   // TMA destinations are 128-byte aligned
+        tma::prefetch_map(&tm.f);
+        tma::prefetch_map(&tm.ws);
+        tma::mbar_init(&mbar, 1);
+        tma::fence_mbar_init();
+    }
+    uint32_t phase = 0;
+    // thread 0: copy the input tile of (isA, w, idx, bt) into F (two boxes of 256 rows)
+    auto issue = [&](int isA, int w, int idx, int bt) {
+        tma::fence_proxy_async();
+        tma::mbar_expect_tx(&mbar, TILE_BYTES);
+        if (isA) {
+            const int x = idx * AC, y = w * D;
+            tma::load_2d(F, &tm.f, x, y, &mbar);
+            if (D > 256) tma::load_2d(F + 256 * 8, &tm.f, x, y + 256, &mbar);
+        } else {
+            const int x = idx * 16 + 8 * bt, y = (w % A.S) * M;
+            tma::load_2d(F, &tm.ws, x, y, &mbar);
+            if (D > 256) tma::load_2d(F + 256 * 8, &tm.ws, x, y + 256, &mbar);
+        }
+    };
+    // every thread: wait for the tile, then take its column s8, rows h8 + 16 k
+    float2 pre[R1];
+    auto take = [&]() {
+        tma::mbar_wait(&mbar, phase);
+        phase ^= 1;
+#pragma unroll
+        for (int k = 0; k < R1; ++k) pre[k] = F[(h8 + 16 * k) * 8 + s8];
+    };
+    auto load_g = [&](int j0, int h, int b) {
+        const float4* G4 = A.Gp + ((int64_t)((j0 / AC) * 4 + h) * (R1 / 2)) * 128 + h8 * 8 + s8;
+#pragma unroll
+        for (int kp = 8 * b; kp < 8 * b + 8 && kp < R1 / 2; ++kp) {
+            const float4 g = (A.dbg & 32) ? make_float4(1.f, 0.f, 1.f, 0.f) : ldg_na(G4 + kp * 128);
+            pre[2 * kp] = make_float2(g.x, g.y);
+            pre[2 * kp + 1] = make_float2(g.z, g.w);
+        }
+    };
+    int pnext = -1;
+    // thread 0 (after the tile's first exchange barrier: F is free): publish the next job and,
+    // when its inputs may be read now, start their copy
+    auto claim_issue = [&]() {
+        int isA0, idx0, w0, ready = 0;
+        if (decode(pnext, A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
+            const int gen0 = w0 / A.S, slot0 = w0 - gen0 * A.S;
+            ready = isA0 || (A.dbg & 1) || ld_acquire(doneA + slot0) >= (gen0 + 1) * A.nA;
+            if (ready) issue(isA0, w0, idx0, 0);
+        }
+        jobsm[0] = pnext;
+        jobsm[1] = ready;
+    };
+    int* pend = nullptr;
+    auto flush = [&]() {
+        if (pend) {
+            __threadfence();
+            atomicAdd(pend, 1);
+            pend = nullptr;
+        }
+    };
+    if (tid == 0) {
+        jobsm[0] = atomicAdd(queue, 1);
+        jobsm[1] = 0;
+    }
+    __syncthreads();
+    for (;;) {
+        const int pref = jobsm[1];
+        if (tid == 0) {
+            int isA0, idx0, w0;
+            if (decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
+                jobdec[0] = isA0; jobdec[1] = w0; jobdec[2] = idx0;
+            } else {
+                jobdec[0] = -1;
+            }
+        }
+        __syncthreads();
+        const int isA = jobdec[0];
+        if (isA < 0) break;
+        const int w = jobdec[1], idx = jobdec[2];
+        const int gen = w / A.S, slot = w - gen * A.S;
+        float2* wsl = A.ws + (int64_t)slot * MQD;
+        if (tid == 0) {
+            if (!(A.dbg & 1)) {
+                const int* cnt = isA ? doneB + slot : (pref ? nullptr : doneA + slot);
+                const int target = isA ? gen * A.nB : (gen + 1) * A.nA;
+                if (cnt && ld_acquire(cnt) < target) {
+                    flush();
+                    spin_until(cnt, target);
+                }
+            }
+            if (!pref) issue(isA, w, idx, 0);   // (B: after the dependency spin)
+        }
+        take();
+        if (isA) {
+            const int j0 = idx * AC;
+            tile(pre, s8, h8, [&] { if (tid == 0) flush(); },
+                 [&] {
+                     load_g(j0, 0, 0);
+                     if (FULLPF && R1 > 16) load_g(j0, 0, 1);
+                 },
+                 [&](int r, const float2* y) {
+#pragma unroll
+                     for (int m2 = 0; m2 < 16; ++m2) F[s8 * K::FS + 16 * r + h8 + R1 * m2] = y[m2];
+                 },
+                 [] {});
+            __syncthreads();   // F complete; X free
+            const int wq = tid >> 5, ln = tid & 31;
+            const int colM = wq >> 1, uM = ln >> 3, iM = (ln & 7) + 8 * (wq & 1);
+#pragma unroll 1
+            for (int h = 0; h < 4; ++h) {
+                const int fcol = 2 * h + (s8 >> 2);
+                const int jS = j0 + fcol;
+                const int sig = (int)((((int64_t)jS * A.beta - ((int64_t)A.Kmod * jS) % D) % D + D) % D);
+                if (h == 3 && tid == 0) pnext = atomicAdd(queue, 1);
+                const float2* Fc = F + fcol * K::FS;
+                const int e0 = (sig - h8) & (D - 1);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
+                if (R1 > 16) {
+                    if (!FULLPF) {
+                        asm volatile("" ::: "memory");
+                        load_g(j0, h, 1);
+                    }
+#pragma unroll
+                    for (int k = 16; k < R1; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
+                }
+                if (!XDB || h == 3) __syncthreads();   // previous tile's readers are done with X; (h = 3) F is dead
+                if (h == 3 && tid == 0) claim_issue();
+                const int jM = j0 + 2 * h + colM;
+                const int kap = ((jM / A.c - uM) % Q + Q) % Q;
+                float2* dst = wsl + (int64_t)jM * (Q * D) + (iM >> 2) * 16 + (iM & 3) * 4 + kap;
+                tile(pre, 4 * colM + uM, iM, [] {},
+                     [&] {
+                         if (h < 3) {
+                             load_g(j0, h + 1, 0);
+                             if (FULLPF && R1 > 16) load_g(j0, h + 1, 1);
+                         }
+                     },
+                     [&](int r, const float2* y) {
+                         if (A.dbg & (4 | 128)) return;
+#pragma unroll
+                         for (int m2 = 0; m2 < 16; ++m2) dst[(4 * r + (R1 / 4) * m2) * 16] = y[m2];
+                     },
+                     [] {});
+            }
+            if (tid == 0) pend = doneA + slot;
+        } else {
+#pragma unroll 1
+            for (int bt = 0; bt < BT; ++bt) {
+                if (bt == BT - 1 && tid == 0) pnext = atomicAdd(queue, 1);
+                const int n = idx * 16 + 8 * bt + s8;
+                const float2 e = ldg_na2(A.E + n);
+                float2* dst = A.out + (int64_t)w * M * N + n;
+                if (bt) {
+                    if (!XDB) __syncthreads();   // previous tile's readers are done with X
+                    take();
+                }
+                tile(pre, s8, h8, [&] { if (tid == 0) flush(); }, [] {},
+                     [&](int r, const float2* y) {
+                         if (A.dbg & (4 | 64)) return;
+#pragma unroll
+                         for (int m2 = 0; m2 < 16; ++m2) {
+                             const int m = 16 * r + h8 + R1 * m2;
+                             __stcs(dst + m * N, cmw(y[m2], e));
+                         }
+                     },
+                     [&] {   // F free: the next tile's copy
+                         if (tid == 0) {
+                             if (bt + 1 < BT) issue(0, w, idx, bt + 1);
+                             else claim_issue();
+                         }
+                     });
+            }
+#pragma unroll
+            for (int j = tid; j < M; j += K::NT)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(wsl + (int64_t)j * (Q * D) + idx * 16) : "memory");
+            if (tid == 0) pend = doneB + slot;
+        }
+    }
+    __syncthreads();
     if (tid == 0) flush();
 }
 

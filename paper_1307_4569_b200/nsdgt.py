@@ -143,8 +143,11 @@ class Plan:
         [0, ceil(Lg/2)) are times 0.., the rest negative times) and the plan is a shear-OLA plan
         (dgt_plan_fir) with block length ``Lb`` (0 = automatic)."""
         import torch
-        self.dtype = dtype
         code = _dtype_code(dtype)
+        # canonical name: every numpy / torch dtype below derives from the code, never from the
+        # alias the caller passed ("complex64", "fp32", ...)
+        self.dtype = "c64" if code == DGT_C64 else "c128"
+        self._np_c = np.complex64 if code == DGT_C64 else np.complex128
         self._cdt = torch.complex64 if code == DGT_C64 else torch.complex128
         self._rdt = torch.float32 if code == DGT_C64 else torch.float64
         self.real_input = bool(real_input)
@@ -258,7 +261,7 @@ class Plan:
     def dual_window(self, tight: bool = False, stream=None) -> np.ndarray:
         """Canonical dual (S^{-1} g) or tight (S^{-1/2} g) window of the plan's window on its
         lattice, computed on the GPU (dgt_window_dual); returned as a host numpy array."""
-        out = np.empty(self.L, dtype=np.complex64 if self.dtype == "c64" else np.complex128)
+        out = np.empty(self.L, dtype=self._np_c)
         _check(_lib.dgt_window_dual(self._h, 1 if tight else 0, ctypes.c_void_p(out.ctypes.data), DGT_G_ON_HOST,
                                     _stream_ptr(stream)), "dgt_window_dual")
         return out
@@ -289,7 +292,7 @@ class Plan:
             if f2.ndim != 2 or f2.shape[1] != self.L:
                 raise ValueError(f"f must have shape (W, {self.L})")
             fptr, W = f2.ctypes.data, f2.shape[0]
-            np_c = np.complex64 if self.dtype == "c64" else np.complex128
+            np_c = self._np_c
             if out is None:
                 out = np.empty((W, self.M, self.N), dtype=np_c)
             elif (out.dtype != np_c or not out.flags.c_contiguous or out.size != W * self.M * self.N

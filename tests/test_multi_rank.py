@@ -74,3 +74,33 @@ def test_two_rank_gloo_shard_gather_reduce():
     assert err == 0.0          # sharded results gathered in order equal the single-process result
     assert tmax == 2.0         # MAX over ranks (device time is the max over ranks)
     assert tsum == 5.0         # every signal processed exactly once
+
+
+def _bench_dry_run(*extra):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", *extra],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout   # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_bench_spawns_ranks_weak():
+    """`python bench.py --gpus 2` without torchrun re-executes itself with 2 ranks (gloo on CPU);
+    weak scaling: every rank its own W signals, disjoint."""
+    d = _bench_dry_run()
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    shards = sorted((r, a, b) for r, a, b in d["shards"])
+    assert [r for r, _, _ in shards] == [0, 1]
+    assert shards[0][1:] == (0, 1024) and shards[1][1:] == (1024, 2048)
+
+
+def test_bench_spawns_ranks_strong():
+    d = _bench_dry_run("--scaling", "strong")
+    shards = sorted((r, a, b) for r, a, b in d["shards"])
+    assert shards[0][1:] == (0, 512) and shards[1][1:] == (512, 1024)
