@@ -30,6 +30,8 @@ __global__ void k_window_factor(cx<T>* G, const double2* gt, int64_t L, int64_t 
 struct FastPlan {
     int kind = 0;  // 0 = none (generic path); 2 = fused persistent kernel (fused8, or fused7)
     int xdb = 0;   // fused7t: double-buffered exchange (NSDGT_XDB=1)
+    int early = 0; // fused7 D = 512: half-tile-early prefetch (NSDGT_EARLY=1)
+    int gpersist = 0;   // experiment: G' in a persisting L2 access-policy window (NSDGT_GPERSIST=1)
     int ver = 7;   // forward kernel: 7 = fused7 (default), 9 = fused7t (TMA tile loads), 8 = fused8 (NSDGT_FUSED)
     const char* name = "none";
     int D = 0, MM = 0, Q = 0, c = 0, N = 0;
@@ -55,6 +57,9 @@ struct FastPlan {
 template <int D, int MINB>
 static void launch7(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
     v7::fused7_kernel<D, MINB><<<grid, v7::Cfg<D>::NT, smem, st>>>(a);
+}
+static void launch7e(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
+    v7::fused7_kernel<512, 3, true, false, true><<<grid, v7::Cfg<512>::NT, smem, st>>>(a);
 }
 // real input (promoted on load): the default CTAs-per-SM variants only
 template <int D, int MINB>
@@ -146,6 +151,11 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     int minb = v8k ? 2 : D == 512 ? 3 : 5;
     if (const char* e = std::getenv("NSDGT_CTAS"))
         minb = v8k ? std::max(2, std::min(D == 512 ? 2 : 3, std::atoi(e))) : std::max(3, std::min(D == 512 ? 4 : 5, std::atoi(e)));
+    fp->early = (fp->ver == 7 && D == 512 && minb == 3 && std::getenv("NSDGT_EARLY") && std::atoi(std::getenv("NSDGT_EARLY"))) ? 1 : 0;
+    if (fp->early &&
+        cudaFuncSetAttribute((const void*)v7::fused7_kernel<512, 3, true, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v7::Cfg<512>::SMEM) != cudaSuccess)
+        return DGT_ECUDA;
     {
         const void* ka = D == 512 ? (const void*)v7::fused7a_kernel<512, 3> : (const void*)v7::fused7a_kernel<256, 5>;
         const size_t sm = D == 512 ? v7::Cfg<512>::SMEM : v7::Cfg<256>::SMEM;
@@ -251,6 +261,8 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
         fp->grid_real = std::min(per_sm * sms, per_sm_r * sms);
     }
     fp->dbg = std::getenv("NSDGT_DBG") ? std::atoi(std::getenv("NSDGT_DBG")) : 0;   // experiment knobs
+    fp->gpersist = std::getenv("NSDGT_GPERSIST") ? std::atoi(std::getenv("NSDGT_GPERSIST")) : 0;
+    if (fp->gpersist) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)M * Q * D * 8);
     if (fp->dbg & 16) {   // phase trace of a -DNSDGT_TRACE build (tools/v7trace.py, dgt_debug_trace_log)
         if (cudaMalloc(&fp->tracelog, sizeof(unsigned long long) * 8 * 4096) != cudaSuccess) return DGT_ENOMEM;
     }
@@ -298,6 +310,15 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
         cudaMemsetAsync(fp->tracelog, 0, sizeof(unsigned long long) * 8 * 4096, st);
         a.log = fp->tracelog;
     }
+    if (fp->gpersist) {   // experiment: keep G' resident (the ring and c stream normally)
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.base_ptr = fp->Gp;
+        v.accessPolicyWindow.num_bytes = (size_t)fp->MM * fp->Q * fp->D * 8;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+    }
     if (fp->ver == 9 && !real_in) {
         v7::Maps m;
         const int64_t D = fp->D, M = fp->MM, Q = fp->Q;
@@ -320,9 +341,15 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
         if (fp->D == 512) launch7r<512, 3>(a, fp->grid_real, fp->smem, st);
         else launch7r<256, 5>(a, fp->grid_real, fp->smem, st);
     } else if (fp->D == 512) {
-        (fp->minb == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st);
+        if (fp->early) launch7e(a, fp->grid, fp->smem, st);
+        else (fp->minb == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st);
     } else {
         (fp->minb == 5 ? launch7<256, 5> : fp->minb == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st);
+    }
+    if (fp->gpersist) {
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
     }
     return DGT_OK;
 }

@@ -188,7 +188,7 @@ struct Args {
     int dbg;             // experiment knobs (0 in production; results are wrong with all but 16):
                          // 1 no dependency spin, 4 no global stores, 8 no DFT arithmetic,
                          // 16 phase trace (-DNSDGT_TRACE builds), 32 no G' loads,
-                         // 64 no c stores, 128 no ring stores
+                         // 64 no c stores, 128 no ring stores, 256 skip B jobs, 512 skip A jobs
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -284,10 +284,10 @@ __device__ __forceinline__ int xslot(int s) { return (((s & 1) << 2) | (s >> 1))
 struct NoMid {
     __device__ void operator()() const {}
 };
-template <int D, class Before, class After, class Emit, class Mark, class Mid = NoMid>
+template <int D, class Before, class After, class Emit, class Mark, class Mid = NoMid, class After0 = NoMid>
 __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2, int s1, int t, int os, int oi,
                                          Before&& before_sync, After&& after_sync, Emit&& emit, int dbg, Mark&& mark,
-                                         Mid&& mid = Mid()) {
+                                         Mid&& mid = Mid(), After0&& after0 = After0()) {
     constexpr int R1 = Cfg<D>::R1, NR = Cfg<D>::NR;
     mark(10);
     if (!(dbg & 8)) dftR<R1>(v);
@@ -316,6 +316,7 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
         for (int tt = 0; tt < 16; ++tt) y[tt] = xr[tt];
         if (r + 1 < NR) __syncthreads();   // round r + 1 reuses the buffer
         if (r == NR - 1) after_sync();
+        else after0();   // (NR = 2) v[0..15] are dead: the first half of the next tile may load
         if (!(dbg & 8)) dft16(y);
         emit(r, y);
     }
@@ -362,7 +363,10 @@ __device__ __forceinline__ void dft_tile_db(float2* v, const float2* tw, float2*
 
 // FULLPF: the whole next tile's inputs are prefetched behind the current tile's stage 2
 // (fits the 168-register budget of 3 CTAs/SM; with 4+ CTAs only the first half).
-template <int D, int MINB, bool FULLPF = (MINB <= 3), bool REAL = false>
+// EARLY (D = 512): the first half of the next tile's inputs is loaded after the first exchange
+// round (its registers v[0..15] are dead then), the second half after the last round -- half
+// a tile more time in flight than loading both halves at the end.
+template <int D, int MINB, bool FULLPF = (MINB <= 3), bool REAL = false, bool EARLY = false>
 __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     using K = Cfg<D>;
     constexpr int R1 = K::R1, Q = K::Q, M = D, AC = K::ACOL, BT = K::BT;
@@ -453,9 +457,13 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
     auto prefetch_next = [&]() {
         int isA0, idx0, w0;
         if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
-            load_first(isA0, w0, idx0, 0);
-            if (FULLPF && R1 > 16) load_first(isA0, w0, idx0, 1);
+            if (!EARLY) load_first(isA0, w0, idx0, 0);
+            if ((FULLPF || EARLY) && R1 > 16) load_first(isA0, w0, idx0, 1);
         }
+    };
+    auto prefetch_next0 = [&]() {   // EARLY: the first half
+        int isA0, idx0, w0;
+        if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) load_first(isA0, w0, idx0, 0);
     };
     // Completion signals are deferred: thread 0 publishes "job done" (fence + counter add)
     // once it is into its next job's first tile, when the job's stores have drained and
@@ -506,6 +514,17 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
         mark(4);
         // B inputs may be read only after the spin.  (A jobs: thread 0's spin precedes its
         // first exchange barrier, hence every ring store.)
+        if ((isA && (A.dbg & 512)) || (!isA && (A.dbg & 256))) {   // experiment: skip this job kind
+            if (tid == 0) {
+                flush();
+                pend = (isA ? doneA : doneB) + slot;
+                pnext = atomicAdd(queue, 1);
+                jobsm[0] = pnext;
+                jobsm[1] = 0;
+            }
+            __syncthreads();
+            continue;
+        }
         if (!pref) {
             if (!isA) __syncthreads();
             load_first(isA, w, idx, 0);
@@ -518,15 +537,16 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
             // Zak DFT of 8 columns: F_j(nu), nu = 16 r + i + R1 m2, stored at F[col * FS + nu]
             dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, [&] { if (tid == 0) flush(); },
                         [&] {
-                            load_g(j0, 0, 0);
-                            if (FULLPF && R1 > 16) load_g(j0, 0, 1);
+                            if (!EARLY) load_g(j0, 0, 0);
+                            if ((FULLPF || EARLY) && R1 > 16) load_g(j0, 0, 1);
                         },
                         [&](int r, const float2* y) {
 #pragma unroll
                             for (int m2 = 0; m2 < 16; ++m2) {
                                 F[s8 * K::FS + 16 * r + h8 + R1 * m2] = y[m2];
                             }
-                        }, A.dbg, mark);
+                        }, A.dbg, mark, NoMid(),
+                        [&] { if (EARLY) load_g(j0, 0, 0); });
             mark(20);
             __syncthreads();   // F complete; X free
             mark(21);
@@ -572,8 +592,8 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                             [&] { if (h == 3 && tid == 0) claim_ready(); },
                             [&] {
                                 if (h < 3) {
-                                    load_g(j0, h + 1, 0);
-                                    if (FULLPF && R1 > 16) load_g(j0, h + 1, 1);
+                                    if (!EARLY) load_g(j0, h + 1, 0);
+                                    if ((FULLPF || EARLY) && R1 > 16) load_g(j0, h + 1, 1);
                                 } else {
                                     prefetch_next();
                                 }
@@ -582,7 +602,13 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                                 if (A.dbg & (4 | 128)) return;
 #pragma unroll
                                 for (int m2 = 0; m2 < 16; ++m2) dst[(4 * r + (R1 / 4) * m2) * 16] = y[m2];
-                            }, A.dbg, mark);
+                            }, A.dbg, mark, NoMid(),
+                            [&] {
+                                if (EARLY) {
+                                    if (h < 3) load_g(j0, h + 1, 0);
+                                    else prefetch_next0();
+                                }
+                            });
             }
             if (tid == 0) pend = doneA + slot;
         } else {
@@ -606,8 +632,8 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                             },
                             [&] {
                                 if (bt + 1 < BT) {
-                                    load_ring(w, idx, bt + 1, 0);
-                                    if (FULLPF && R1 > 16) load_ring(w, idx, bt + 1, 1);
+                                    if (!EARLY) load_ring(w, idx, bt + 1, 0);
+                                    if ((FULLPF || EARLY) && R1 > 16) load_ring(w, idx, bt + 1, 1);
                                 } else {
                                     prefetch_next();
                                 }
@@ -619,7 +645,13 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                                     const int m = 16 * r + h8 + R1 * m2;
                                     __stcs(dst + m * N, cmw(y[m2], e));
                                 }
-                            }, A.dbg, mark);
+                            }, A.dbg, mark, NoMid(),
+                            [&] {
+                                if (EARLY) {
+                                    if (bt + 1 < BT) load_ring(w, idx, bt + 1, 0);
+                                    else prefetch_next0();
+                                }
+                            });
             }
             // The ring lines this job read are dead (this job is their only reader; the
             // exchange barriers ordered every load before this point): drop them from L2 so

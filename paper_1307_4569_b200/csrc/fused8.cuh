@@ -211,6 +211,17 @@ __global__ void __launch_bounds__(256, MINB) fused8_kernel(Args A) {
                 spin_until(cnt, target);
             }
         }
+        if ((isA && (A.dbg & 512)) || (!isA && (A.dbg & 256))) {   // experiment: skip this job kind
+            if (tid == 0) {
+                flush();
+                pend = (isA ? doneA : doneB) + slot;
+                pnext = atomicAdd(queue, 1);
+                jobsm[0] = pnext;
+                jobsm[1] = 0;
+            }
+            __syncthreads();
+            continue;
+        }
         if (!pref) {
             if (!isA) __syncthreads();   // B inputs only after the dependency spin
             load_first(isA, w, idx);
