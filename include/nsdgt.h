@@ -124,6 +124,22 @@ int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t lambda1, 
 int dgt_plan_fir(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t lambda1, int64_t lambda2,
                  const void* g, int64_t Lg, int64_t Lb, int dtype, int flags, void* cuda_stream);
 
+/* Multiwindow plan (the comparison algorithm of, Sec. 3.1):
+ * the same transform Eq. (DGT) on the lattice (a, M, lambda1/lambda2), computed through the
+ * co-set decomposition of Prop. mwindec -- lambda2 separable DGTs on the lattice (lambda2 a, b)
+ * with the windows g_m = M_{m s mod b} T_{m a} g, m < lambda2, joined by the phases of
+ * Eq. (mw_phases): c(k, n) = exp(-2 pi i nt (lambda2 a) (m s mod b) / L) d_m(k, nt) for
+ * n = nt lambda2 + m (reading Z12: m = n mod lambda2).  Its cost grows linearly with lambda2,
+ * the shear algorithm's does not (Fig. 2).  The windows g_m are made on the
+ * host in fp64 (exact integer phase indices), rounded once to dtype; each inner transform runs
+ * the plan path of dgt_plan for its separable lattice.  Arguments as dgt_plan (flags:
+ * DGT_REAL_INPUT, DGT_G_ON_HOST, DGT_FORCE_GENERIC).  The returned plan runs dgt_execute /
+ * dgt_execute_host / dgt_plan_query (kernel_path = 32 + the inner plans' path) / dgt_destroy;
+ * dgt_execute_inverse and dgt_window_dual return DGT_EUNSUPPORTED.
+ * Errors: as dgt_plan. */
+int dgt_plan_multiwindow(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t lambda1, int64_t lambda2,
+                         const void* g, int dtype, int flags, void* cuda_stream);
+
 /* c = DGT(f) for W signals.  f: device, W x L (complex, or real with DGT_REAL_INPUT),
  * signal-major.  c: device, W x M x N complex, n fastest (c[(w*M + m)*N + n]).  Fully
  * overwritten.  Asynchronous and stream-ordered on cuda_stream; allocates nothing.
@@ -136,9 +152,9 @@ int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_s
  * i.e. the adjoint of dgt_execute.  A plan built with the canonical dual window S^{-1} g
  * inverts the DGT of a plan built with g.  c: device, W x M x N complex (n fastest), read
  * only.  f: device, W x L complex of the plan's dtype (always complex, also for
- * DGT_REAL_INPUT plans), fully overwritten.  Asynchronous and stream-ordered; the first call
- * allocates the plan's synthesis workspace (kept until dgt_destroy).  Runs the generic
- * (adjoint) kernels for every lattice.  W = 0 is a no-op.
+ * DGT_REAL_INPUT plans), fully overwritten.  Asynchronous and stream-ordered; allocates nothing
+ * (the synthesis workspace is made by dgt_plan).  Runs the fused adjoint kernel on the fused
+ * lattices and the generic (adjoint) kernels elsewhere.  W = 0 is a no-op.
  * Errors: DGT_EINVAL (null/aliasing, W < 0), DGT_ECUDA, DGT_ECUFFT, DGT_ENOMEM. */
 int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void* cuda_stream);
 
@@ -158,8 +174,10 @@ int dgt_window_dual(dgt_plan_t plan, int kind, void* out, int flags, void* cuda_
 
 /* End-to-end variant with HOST buffers: copies f (host, W x L) to the device, runs the
  * transform and copies c (host, W x M x N) back, chunk by chunk with the copies overlapped
- * on two extra streams.  Returns after c is complete on the host (synchronous).  Staging
- * buffers are allocated on first use and kept by the plan.  Errors: as dgt_execute, DGT_ENOMEM. */
+ * on two extra streams.  Returns after c is complete on the host (synchronous), also on an
+ * error once a copy was enqueued (the caller may reuse its buffers on return).  The staging
+ * buffers (two slots of ~64 MB of output) and copy streams are made by the plan constructors;
+ * this call allocates nothing.  Errors: as dgt_execute. */
 int dgt_execute_host(dgt_plan_t plan, const void* f_host, void* c_host, int64_t W, void* cuda_stream);
 
 /* Release everything the plan owns.  The caller must have synchronised its streams. */

@@ -1211,6 +1211,27 @@ __global__ void k_ola_add(cx<T>* c, const cx<T>* cb, int64_t M, int64_t N, int64
     }
 }
 
+// Multiwindow DGT, Eq. (mw_phases) of PAPER.md:397-403: with n = nt lambda2 + m (m < lambda2;
+// reading Z12: m = n mod lambda2), at = lambda2 a and sigma_m = m s mod b,
+//   c[w][k][n] = exp(-2 pi i nt at sigma_m / L) d_m[w][k][nt],
+// d_m the separable DGT of f with g_m = M_{sigma_m} T_{m a} g on (at, b).  The phase index
+// (nt at mod L) sigma_m mod L is exact in int64 (nt at < L, sigma_m < b <= L < 2^31).
+template <typename T>
+__global__ void k_mw_interleave(cx<T>* c, const cx<T>* d, const int64_t* sig, int64_t Wc, int64_t M, int64_t N,
+                                int64_t l2, int64_t at, int64_t L, int64_t total) {
+    const int64_t Nt = N / l2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = i % N, wk = i / N;
+        const int64_t m = n % l2, nt = n / l2;
+        const int64_t r = (((nt * at) % L) * sig[m]) % L;
+        double sn, cs;
+        sincospi(-2.0 * (double)r / (double)L, &sn, &cs);
+        const cx<T> v = d[(m * Wc * M + wk) * Nt + nt];
+        const T pr = (T)cs, pi = (T)sn;
+        c[i] = mk<T>(v.x * pr - v.y * pi, v.x * pi + v.y * pr);
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // the plan
 // ---------------------------------------------------------------------------------
@@ -1251,6 +1272,13 @@ struct Plan {
     // through the inner plan; their coefficients are overlap-added
     struct Plan* ola = nullptr;
     int64_t ola_Lb = 0, ola_Nb = 0, ola_Ws = 0, ola_pmin = 0, ola_pmax = 0;
+    // multiwindow plan (dgt_plan_multiwindow): lambda2 separable
+    // plans on (lambda2 a, M) with the windows g_m, a [lambda2][Wc][M][N / lambda2] buffer of
+    // their coefficients and the residues sigma_m = m s mod b (device)
+    std::vector<struct Plan*> mw;
+    int64_t mw_Wc = 0;
+    void* mw_d = nullptr;
+    int64_t* mw_sig = nullptr;
     void* ola_x = nullptr;   // [Ws Nb][Lx] blocks (input type)
     void* ola_c = nullptr;   // [Ws Nb][M][Nx] block coefficients
     int gA = 0, gB = 0;      // Zak / output kernels with per-CTA buffers in global scratch
@@ -1290,10 +1318,10 @@ struct Plan {
 };
 
 enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_ZAKADJ = 6,
-                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_COUNT = 9 };
+                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_COUNT = 10 };
 static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
                                            "zak_ct", "out_f4096", "zak_adjoint", "out_adjoint",
-                                           "fused7a_t_p1"};
+                                           "fused7a_t_p1", "multiwindow_interleave"};
 
 static cudaEvent_t prof_event(Plan* P) {
     if (P->pool_used == P->pool.size()) {
@@ -1325,6 +1353,9 @@ static void prof_close(Plan* P, int h, int kind, double bytes, double flops, cud
 static void free_plan(Plan* P) {
     if (!P) return;
     if (P->ola) free_plan(P->ola);
+    for (Plan* Q : P->mw) free_plan(Q);
+    if (P->mw_d) cudaFree(P->mw_d);
+    if (P->mw_sig) cudaFree(P->mw_sig);
     if (P->ola_x) cudaFree(P->ola_x);
     if (P->ola_c) cudaFree(P->ola_c);
     if (P->inv_alias & 1) P->Cinv = nullptr;
@@ -1898,9 +1929,41 @@ static int execute_ola(Plan* P, const void* f, void* c, int64_t W, cudaStream_t 
     return DGT_OK;
 }
 
+static int execute(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st);
+
+// multiwindow: per chunk of Wc signals, the lambda2 separable transforms into mw_d, then the
+// phase / interleave kernel into c
+static int execute_mw(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) {
+    const dgt_lattice_info& I = P->info;
+    const int64_t l2 = (int64_t)P->mw.size(), Nt = I.N / l2;
+    const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
+    for (int64_t w0 = 0; w0 < W; w0 += P->mw_Wc) {
+        const int64_t wc = std::min<int64_t>(P->mw_Wc, W - w0);
+        const char* fw = (const char*)f + (size_t)w0 * I.L * ein;
+        for (int64_t m = 0; m < l2; ++m) {
+            char* dm = (char*)P->mw_d + (size_t)m * P->mw_Wc * I.M * Nt * P->esz;
+            int rc = execute(P->mw[m], fw, dm, wc, st);
+            if (rc) return rc;
+        }
+        const int64_t tot = wc * I.M * I.N;
+        char* cw = (char*)c + (size_t)w0 * I.M * I.N * P->esz;
+        const int ph = prof_open(P, st);
+        if (P->dtype == DGT_C64)
+            k_mw_interleave<float><<<grid_for(tot), 256, 0, st>>>((float2*)cw, (const float2*)P->mw_d, P->mw_sig,
+                                                                  P->mw_Wc, I.M, I.N, l2, l2 * I.a, I.L, tot);
+        else
+            k_mw_interleave<double><<<grid_for(tot), 256, 0, st>>>((double2*)cw, (const double2*)P->mw_d, P->mw_sig,
+                                                                   P->mw_Wc, I.M, I.N, l2, l2 * I.a, I.L, tot);
+        prof_close(P, ph, PK_MW, 2.0 * tot * P->esz, 6.0 * tot, st);
+        CUDA_TRY(cudaGetLastError());
+    }
+    return DGT_OK;
+}
+
 static int execute(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
     if (P->ola) return execute_ola(P, f, c, W, st);
+    if (!P->mw.empty()) return execute_mw(P, f, c, W, st);
     const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
     if (I.branch == DGT_BRANCH_FREQ && !P->fast) {
         // front batches of P->fb signals (a multiple of the chunk), then the chunks of each
@@ -1968,8 +2031,11 @@ int dgt_lattice_plan(int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, in
 
 static int alloc_host_staging(Plan* P);
 
-int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int dtype,
-             int flags, int64_t max_chunk, int force_shear, int64_t s0, int64_t s1, void* cuda_stream) {
+// The plan of dgt_plan; staging = make the host-buffer staging of dgt_execute_host (inner plans
+// of the shear-OLA and multiwindow plans are only executed on device buffers and skip it).
+static int make_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int dtype,
+                     int flags, int64_t max_chunk, int force_shear, int64_t s0, int64_t s1, void* cuda_stream,
+                     bool staging) {
     if (!out || !g) return fail(DGT_EINVAL, "null pointer");
     *out = nullptr;
     if (dtype != DGT_C64 && dtype != DGT_C128) return fail(DGT_EINVAL, "bad dtype");
@@ -1996,7 +2062,7 @@ int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64
         P->chunk = max_chunk > 0 ? max_chunk : fast_chunk(&P->fp);
     }
     if (!rc) rc = alloc_workspace(P, P->chunk);
-    if (!rc) rc = alloc_host_staging(P);
+    if (!rc && staging) rc = alloc_host_staging(P);
     if (rc) {
         free_plan(P);
         return rc;
@@ -2006,6 +2072,11 @@ int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64
     P->info.kernel_path = P->fast;
     *out = (dgt_plan_t)P;
     return DGT_OK;
+}
+
+int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int dtype,
+             int flags, int64_t max_chunk, int force_shear, int64_t s0, int64_t s1, void* cuda_stream) {
+    return make_plan(out, L, a, M, l1, l2, g, dtype, flags, max_chunk, force_shear, s0, s1, cuda_stream, true);
 }
 
 int dgt_plan_fir(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int64_t Lg,
@@ -2063,8 +2134,8 @@ int dgt_plan_fir(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, i
         std::memcpy(gx.data() + esz * x, gh.data() + esz * i, esz);
     }
     dgt_plan_t inner = nullptr;
-    rc = dgt_plan(&inner, Lin, a, M, l1, l2, gx.data(), dtype, (flags & ~DGT_G_ON_HOST) | DGT_G_ON_HOST, 0, 0, 0, 0,
-                  cuda_stream);
+    rc = make_plan(&inner, Lin, a, M, l1, l2, gx.data(), dtype, (flags & ~DGT_G_ON_HOST) | DGT_G_ON_HOST, 0, 0, 0, 0,
+                   cuda_stream, !(Lx < L));
     if (rc) return rc;
     if (!blocks) {   // the blocks would be as long as the signal: the full-length plan
         *out = inner;
@@ -2095,6 +2166,92 @@ int dgt_plan_fir(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, i
     P->info.chunk = P->ola_Ws;
     P->info.workspace_bytes = (int64_t)(P->ola_Ws * per_sig) + P->ola->info.workspace_bytes;
     P->info.kernel_path = 16 + P->ola->info.kernel_path;   // 16 + inner path: shear-OLA
+    if (int rs = alloc_host_staging(P)) {
+        free_plan(P);
+        return rs;
+    }
+    *out = (dgt_plan_t)P;
+    return DGT_OK;
+}
+
+int dgt_plan_multiwindow(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g,
+                         int dtype, int flags, void* cuda_stream) {
+    if (!out || !g) return fail(DGT_EINVAL, "null pointer");
+    *out = nullptr;
+    if (dtype != DGT_C64 && dtype != DGT_C128) return fail(DGT_EINVAL, "bad dtype");
+    if (flags & ~(DGT_REAL_INPUT | DGT_G_ON_HOST | DGT_FORCE_GENERIC)) return fail(DGT_EINVAL, "bad flags");
+    dgt_lattice_info info{};
+    std::string err;
+    int rc = plan_lattice(L, a, M, l1, l2, flags, false, 0, 0, &info, &err);
+    if (rc) {
+        if (rc == DGT_EILLEGAL_LENGTH) g_last_lmin = info.L_min;
+        return fail(rc, err);
+    }
+    const size_t esz = dtype == DGT_C64 ? 8 : 16;
+    const int64_t lam2 = info.lambda2, b = info.b, s = info.s, Nt = info.N / lam2;
+    // the window in fp64 on the host
+    std::vector<double2> gh(L);
+    {
+        std::vector<unsigned char> raw(esz * L);
+        if (flags & DGT_G_ON_HOST) std::memcpy(raw.data(), g, esz * L);
+        else CUDA_TRY(cudaMemcpy(raw.data(), g, esz * L, cudaMemcpyDeviceToHost));
+        for (int64_t l = 0; l < L; ++l) {
+            if (dtype == DGT_C64) {
+                const float2 v = ((const float2*)raw.data())[l];
+                gh[l] = make_double2(v.x, v.y);
+            } else {
+                gh[l] = ((const double2*)raw.data())[l];
+            }
+        }
+    }
+    Plan* P = new Plan();
+    P->info = info;
+    P->dtype = dtype;
+    P->flags = flags & ~DGT_G_ON_HOST;
+    P->esz = esz;
+    cudaGetDevice(&P->device);
+    // chunk: the coefficient buffer of the lambda2 inner transforms stays near 256 MB
+    P->mw_Wc = std::max<int64_t>(1, std::min<int64_t>(kMaxChunk, (int64_t)((256ull << 20) / ((size_t)M * info.N * esz))));
+    std::vector<int64_t> sig(lam2);
+    std::vector<unsigned char> gm(esz * L);
+    for (int64_t m = 0; m < lam2; ++m) {
+        // g_m = M_{sigma_m} T_{m a} g, sigma_m = m s mod b (Prop. mwindec / Eq. mw_phases):
+        // g_m(l) = exp(2 pi i (sigma_m l mod L) / L) g((l - m a) mod L), exact integer phase index
+        sig[m] = (m * s) % b;
+        for (int64_t l = 0; l < L; ++l) {
+            const int64_t r = (int64_t)(((__int128)sig[m] * l) % L);
+            const long double th = 2.0L * 3.141592653589793238462643383279502884L * (long double)r / (long double)L;
+            const double c0 = (double)cosl(th), s0 = (double)sinl(th);
+            const double2 v = gh[(((l - m * a) % L) + L) % L];
+            const double re = v.x * c0 - v.y * s0, im = v.x * s0 + v.y * c0;
+            if (dtype == DGT_C64) ((float2*)gm.data())[l] = make_float2((float)re, (float)im);
+            else ((double2*)gm.data())[l] = make_double2(re, im);
+        }
+        dgt_plan_t inner = nullptr;
+        rc = make_plan(&inner, L, lam2 * a, M, 0, 1, gm.data(), dtype, (flags & ~DGT_G_ON_HOST) | DGT_G_ON_HOST,
+                       P->mw_Wc, 0, 0, 0, cuda_stream, false);
+        if (rc) {
+            free_plan(P);
+            return rc;
+        }
+        P->mw.push_back((Plan*)inner);
+    }
+    if (cudaMalloc(&P->mw_d, (size_t)lam2 * P->mw_Wc * M * Nt * esz) != cudaSuccess ||
+        cudaMalloc(&P->mw_sig, sizeof(int64_t) * lam2) != cudaSuccess ||
+        cudaMemcpy(P->mw_sig, sig.data(), sizeof(int64_t) * lam2, cudaMemcpyHostToDevice) != cudaSuccess) {
+        free_plan(P);
+        return fail(DGT_ENOMEM, "multiwindow buffers");
+    }
+    P->chunk = P->mw_Wc;
+    P->info.chunk = P->mw_Wc;
+    int64_t ws = (int64_t)lam2 * P->mw_Wc * M * Nt * (int64_t)esz;
+    for (Plan* Q : P->mw) ws += Q->info.workspace_bytes;
+    P->info.workspace_bytes = ws;
+    P->info.kernel_path = 32 + P->mw[0]->info.kernel_path;   // 32 + inner path: multiwindow
+    if (int rs = alloc_host_staging(P)) {
+        free_plan(P);
+        return rs;
+    }
     *out = (dgt_plan_t)P;
     return DGT_OK;
 }
@@ -2117,6 +2274,7 @@ int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void
     Plan* P = (Plan*)plan;
     if (!P) return fail(DGT_EINVAL, "null plan");
     if (P->ola) return fail(DGT_EUNSUPPORTED, "synthesis is not implemented for shear-OLA plans");
+    if (!P->mw.empty()) return fail(DGT_EUNSUPPORTED, "synthesis is not implemented for multiwindow plans");
     if (W < 0) return fail(DGT_EINVAL, "W < 0");
     if (W == 0) return DGT_OK;
     if (!f || !c) return fail(DGT_EINVAL, "null pointer");
@@ -2131,6 +2289,7 @@ int dgt_window_dual(dgt_plan_t plan, int kind, void* out, int flags, void* cuda_
     Plan* P = (Plan*)plan;
     if (!P || !out) return fail(DGT_EINVAL, "null pointer");
     if (P->ola) return fail(DGT_EUNSUPPORTED, "dual windows are not implemented for shear-OLA plans");
+    if (!P->mw.empty()) return fail(DGT_EUNSUPPORTED, "dual windows are not implemented for multiwindow plans");
     if (kind != 0 && kind != 1) return fail(DGT_EINVAL, "kind must be 0 (dual) or 1 (tight)");
     if (flags & ~DGT_G_ON_HOST) return fail(DGT_EINVAL, "bad flags");
     const dgt_lattice_info& I = P->info;
@@ -2335,6 +2494,15 @@ int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W) {
         int64_t n = 0;
         for (int64_t w0 = 0; w0 < W; w0 += P->ola_Ws)
             n += 2 + dgt_launches_per_execute((dgt_plan_t)P->ola, std::min<int64_t>(P->ola_Ws, W - w0) * P->ola_Nb);
+        return n;
+    }
+    if (!P->mw.empty()) {   // per chunk: the lambda2 inner transforms + the interleave kernel
+        int64_t n = 0;
+        for (int64_t w0 = 0; w0 < W; w0 += P->mw_Wc) {
+            const int64_t wc = std::min<int64_t>(P->mw_Wc, W - w0);
+            for (Plan* Q : P->mw) n += dgt_launches_per_execute((dgt_plan_t)Q, wc);
+            n += 1;
+        }
         return n;
     }
     const int64_t chunks = (W + P->chunk - 1) / P->chunk;

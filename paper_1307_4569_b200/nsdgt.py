@@ -43,7 +43,7 @@ class KernelStat(ctypes.Structure):
                 ("bytes", ctypes.c_double), ("flops", ctypes.c_double)]
 
 
-EXPORTS = ["dgt_lattice_plan", "dgt_plan", "dgt_plan_fir", "dgt_execute", "dgt_execute_inverse", "dgt_window_dual", "dgt_execute_host",
+EXPORTS = ["dgt_lattice_plan", "dgt_plan", "dgt_plan_fir", "dgt_plan_multiwindow", "dgt_execute", "dgt_execute_inverse", "dgt_window_dual", "dgt_execute_host",
            "dgt_destroy",
            "dgt_plan_query",
            "dgt_launches_per_execute", "dgt_profile_begin", "dgt_profile_end", "dgt_strerror", "dgt_last_error",
@@ -56,6 +56,8 @@ _lib.dgt_plan.argtypes = [ctypes.POINTER(_P)] + [_I64] * 5 + [_P, _INT, _INT, _I
 _lib.dgt_plan.restype = _INT
 _lib.dgt_plan_fir.argtypes = [ctypes.POINTER(_P)] + [_I64] * 5 + [_P, _I64, _I64, _INT, _INT, _P]
 _lib.dgt_plan_fir.restype = _INT
+_lib.dgt_plan_multiwindow.argtypes = [ctypes.POINTER(_P)] + [_I64] * 5 + [_P, _INT, _INT, _P]
+_lib.dgt_plan_multiwindow.restype = _INT
 _lib.dgt_execute.argtypes = [_P, _P, _P, _I64, _P]
 _lib.dgt_execute.restype = _INT
 _lib.dgt_execute_inverse.argtypes = [_P, _P, _P, _I64, _P]
@@ -138,10 +140,14 @@ class Plan:
     """
 
     def __init__(self, L, a, M, lam1, lam2, g, dtype="c64", real_input=False, max_chunk=0, shear=None,
-                 paper_shear=False, force_generic=False, stream=None, fir=False, Lb=0):
+                 paper_shear=False, force_generic=False, stream=None, fir=False, Lb=0, algorithm="shear"):
         """``fir=True``: ``g`` is an FIR window of len(g) <= L taps in FIR order (entries
         [0, ceil(Lg/2)) are times 0.., the rest negative times) and the plan is a shear-OLA plan
-        (dgt_plan_fir) with block length ``Lb`` (0 = automatic)."""
+        (dgt_plan_fir) with block length ``Lb`` (0 = automatic).  ``algorithm="multiwindow"``:
+        the multiwindow comparison algorithm (dgt_plan_multiwindow) instead of the shear
+        algorithm."""
+        if algorithm not in ("shear", "multiwindow"):
+            raise ValueError(f"bad algorithm {algorithm!r}")
         import torch
         code = _dtype_code(dtype)
         # canonical name: every numpy / torch dtype below derives from the code, never from the
@@ -168,7 +174,12 @@ class Plan:
         self._device = torch.cuda.current_device() if torch.cuda.is_available() else -1
         s0, s1 = shear if shear is not None else (0, 0)
         h = ctypes.c_void_p()
-        if fir:
+        if algorithm == "multiwindow":
+            if fir or shear is not None or paper_shear:
+                raise ValueError("the multiwindow algorithm takes no FIR window or shear")
+            _check(_lib.dgt_plan_multiwindow(ctypes.byref(h), L, a, M, lam1, lam2, ctypes.c_void_p(gptr), code,
+                                             flags & ~DGT_SHEAR_PAPER, _stream_ptr(stream)), "dgt_plan_multiwindow")
+        elif fir:
             Lg = ng
             _check(_lib.dgt_plan_fir(ctypes.byref(h), L, a, M, lam1, lam2, ctypes.c_void_p(gptr), Lg, int(Lb), code,
                                      flags, _stream_ptr(stream)), "dgt_plan_fir")
