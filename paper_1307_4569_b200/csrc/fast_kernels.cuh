@@ -32,6 +32,7 @@ struct FastPlan {
     int xdb = 0;   // fused7t: double-buffered exchange (NSDGT_XDB=1)
     int early = 0; // fused7 D = 512: half-tile-early prefetch (NSDGT_EARLY=1)
     int gpersist = 0;   // experiment: G' in a persisting L2 access-policy window (NSDGT_GPERSIST=1)
+    int cst = 0;        // fused7: TMA coefficient stores (NSDGT_CST=1; measured slower, off by default)
     int ver = 7;   // forward kernel: 7 = fused7 (default), 9 = fused7t (TMA tile loads), 8 = fused8 (NSDGT_FUSED)
     const char* name = "none";
     int D = 0, MM = 0, Q = 0, c = 0, N = 0;
@@ -55,16 +56,21 @@ struct FastPlan {
 };
 
 template <int D, int MINB>
-static void launch7(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
-    v7::fused7_kernel<D, MINB><<<grid, v7::Cfg<D>::NT, smem, st>>>(a);
+static void launch7(const v7::Args& a, const CUtensorMap& cm, int grid, size_t smem, cudaStream_t st) {
+    v7::fused7_kernel<D, MINB><<<grid, v7::Cfg<D>::NT, smem, st>>>(a, cm);
 }
-static void launch7e(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
-    v7::fused7_kernel<512, 3, true, false, true><<<grid, v7::Cfg<512>::NT, smem, st>>>(a);
+static void launch7e(const v7::Args& a, const CUtensorMap& cm, int grid, size_t smem, cudaStream_t st) {
+    v7::fused7_kernel<512, 3, true, false, true><<<grid, v7::Cfg<512>::NT, smem, st>>>(a, cm);
+}
+// TMA coefficient stores (the default occupancy)
+template <int D, int MINB>
+static void launch7c(const v7::Args& a, const CUtensorMap& cm, int grid, size_t smem, cudaStream_t st) {
+    v7::fused7_kernel<D, MINB, (MINB <= 3), false, false, true><<<grid, v7::Cfg<D>::NT, smem, st>>>(a, cm);
 }
 // real input (promoted on load): the default CTAs-per-SM variants only
 template <int D, int MINB>
-static void launch7r(const v7::Args& a, int grid, size_t smem, cudaStream_t st) {
-    v7::fused7_kernel<D, MINB, (MINB <= 3), true><<<grid, v7::Cfg<D>::NT, smem, st>>>(a);
+static void launch7r(const v7::Args& a, const CUtensorMap& cm, int grid, size_t smem, cudaStream_t st) {
+    v7::fused7_kernel<D, MINB, (MINB <= 3), true><<<grid, v7::Cfg<D>::NT, smem, st>>>(a, cm);
 }
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -89,6 +95,20 @@ static bool encode_map_2d(CUtensorMap* m, const void* base, uint64_t cols, uint6
     cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t es[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// 3-D map over the coefficients c[W][M][N] viewed as [W M / R1][R1][N] (m = R1 (m div R1) +
+// m mod R1): boxes of 8 columns x 16 rows m mod R1 x 16 rows m div R1 -- one exchange round
+// of a B tile (CST)
+static bool encode_cmap(CUtensorMap* m, const void* c, int64_t W, int64_t M, int64_t N, int64_t R1) {
+    auto fn = tensor_map_encoder();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)R1, (cuuint64_t)(W * M / R1)};
+    cuuint64_t strides[2] = {(cuuint64_t)N * 8, (cuuint64_t)R1 * N * 8};
+    cuuint32_t box[3] = {8, 16, 16};
+    cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(c), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -152,6 +172,11 @@ int build_fast(FastPlan* fp, const dgt_lattice_info& I, const double2* gt, const
     if (const char* e = std::getenv("NSDGT_CTAS"))
         minb = v8k ? std::max(2, std::min(D == 512 ? 2 : 3, std::atoi(e))) : std::max(3, std::min(D == 512 ? 4 : 5, std::atoi(e)));
     fp->early = (fp->ver == 7 && D == 512 && minb == 3 && std::getenv("NSDGT_EARLY") && std::atoi(std::getenv("NSDGT_EARLY"))) ? 1 : 0;
+    fp->cst = (fp->ver == 7 && !fp->early && D == 512 && minb == 3 &&
+               std::getenv("NSDGT_CST") && std::atoi(std::getenv("NSDGT_CST"))) ? 1 : 0;
+    if (fp->cst && cudaFuncSetAttribute((const void*)v7::fused7_kernel<512, 3, true, false, false, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v7::Cfg<512>::SMEM) != cudaSuccess)
+        return DGT_ECUDA;
     if (fp->early &&
         cudaFuncSetAttribute((const void*)v7::fused7_kernel<512, 3, true, false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v7::Cfg<512>::SMEM) != cudaSuccess)
@@ -337,14 +362,21 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
         } else {
             (fp->minb == 3 ? launch8<256, 3> : launch8<256, 2>)(a, fp->grid, fp->smem, st);
         }
-    } else if (real_in) {   // the real variants are compiled for the default occupancy only
-        if (fp->D == 512) launch7r<512, 3>(a, fp->grid_real, fp->smem, st);
-        else launch7r<256, 5>(a, fp->grid_real, fp->smem, st);
-    } else if (fp->D == 512) {
-        if (fp->early) launch7e(a, fp->grid, fp->smem, st);
-        else (fp->minb == 4 ? launch7<512, 4> : launch7<512, 3>)(a, fp->grid, fp->smem, st);
     } else {
-        (fp->minb == 5 ? launch7<256, 5> : fp->minb == 4 ? launch7<256, 4> : launch7<256, 3>)(a, fp->grid, fp->smem, st);
+        CUtensorMap cm{};
+        const bool cst = fp->cst && !real_in;
+        if (cst && !encode_cmap(&cm, c, W, fp->MM, fp->N, fp->D / 16)) return DGT_ECUDA;
+        if (real_in) {   // the real variants are compiled for the default occupancy only
+            if (fp->D == 512) launch7r<512, 3>(a, cm, fp->grid_real, fp->smem, st);
+            else launch7r<256, 5>(a, cm, fp->grid_real, fp->smem, st);
+        } else if (cst) {
+            launch7c<512, 3>(a, cm, fp->grid, fp->smem, st);
+        } else if (fp->D == 512) {
+            if (fp->early) launch7e(a, cm, fp->grid, fp->smem, st);
+            else (fp->minb == 4 ? launch7<512, 4> : launch7<512, 3>)(a, cm, fp->grid, fp->smem, st);
+        } else {
+            (fp->minb == 5 ? launch7<256, 5> : fp->minb == 4 ? launch7<256, 4> : launch7<256, 3>)(a, cm, fp->grid, fp->smem, st);
+        }
     }
     if (fp->gpersist) {
         cudaStreamAttrValue v{};

@@ -284,10 +284,19 @@ __device__ __forceinline__ int xslot(int s) { return (((s & 1) << 2) | (s >> 1))
 struct NoMid {
     __device__ void operator()() const {}
 };
-template <int D, class Before, class After, class Emit, class Mark, class Mid = NoMid, class After0 = NoMid>
+struct NoBar {
+    __device__ void operator()(int) const {}
+};
+// bar_pre(r) / bar_post(r): every thread, right before / after the exchange barrier of round r
+// SYNC0: the buffer X may still be read by the previous tile: a barrier goes right before the
+// first-round writes -- after the stage-1 DFT and twiddles, so that warps whose inputs arrived
+// early can compute while the others wait (measured neutral against a barrier before the call).
+template <int D, bool SYNC0 = false, class Before, class After, class Emit, class Mark, class Mid = NoMid,
+          class After0 = NoMid, class BarPre = NoBar, class BarPost = NoBar>
 __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2, int s1, int t, int os, int oi,
                                          Before&& before_sync, After&& after_sync, Emit&& emit, int dbg, Mark&& mark,
-                                         Mid&& mid = Mid(), After0&& after0 = After0()) {
+                                         Mid&& mid = Mid(), After0&& after0 = After0(), BarPre&& bar_pre = BarPre(),
+                                         BarPost&& bar_post = BarPost()) {
     constexpr int R1 = Cfg<D>::R1, NR = Cfg<D>::NR;
     mark(10);
     if (!(dbg & 8)) dftR<R1>(v);
@@ -295,20 +304,49 @@ __device__ __forceinline__ void dft_tile(float2* v, const float2* tw, float2* X2
     const float4* tw4 = reinterpret_cast<const float4*>(tw);   // twiddle pairs (m, m + 1)
     float2* xw = X2 + xslot(s1) + t;                           // writer: + 17 m1' (+ round buffer)
     const float2* xr = X2 + xslot(os) + 17 * oi;               // reader: + t (+ round buffer)
+    // Twiddles: each round's 8 pairs are loaded back to back (32 registers) and then used --
+    // loading one pair per use exposed the shared-memory latency (config 5: 5.82 -> 5.63 ms).
+    // With two rounds (D = 512) every value is twiddled in place before the first exchange
+    // barrier, so the second round only stores (5.61 ms); with one round (D = 256) the
+    // twiddles are applied as the values are stored (0.336 against 0.339 ms).
+    if constexpr (NR > 1) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            float4 w2s[8];
+#pragma unroll
+            for (int mp = 0; mp < 8; ++mp) w2s[mp] = lds128_nohoist(tw4 + ((16 * r) >> 1) + mp);
+#pragma unroll
+            for (int m = 0; m < 16; m += 2) {
+                if (r || m) v[16 * r + m] = cmw(v[16 * r + m], make_float2(w2s[m >> 1].x, w2s[m >> 1].y));
+                v[16 * r + m + 1] = cmw(v[16 * r + m + 1], make_float2(w2s[m >> 1].z, w2s[m >> 1].w));
+            }
+            asm volatile("" ::: "memory");
+        }
+    }
+    if constexpr (SYNC0 && NR > 1) __syncthreads();
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
+        if constexpr (NR > 1) {
 #pragma unroll
-        for (int m = 0; m < 16; m += 2) {
-            const float4 w2 = lds128_nohoist(tw4 + ((16 * r + m) >> 1));
-            const float2 a = (r || m) ? cmw(v[16 * r + m], make_float2(w2.x, w2.y)) : v[16 * r];
-            const float2 b = cmw(v[16 * r + m + 1], make_float2(w2.z, w2.w));
-            xw[17 * m] = a;
-            xw[17 * (m + 1)] = b;
-            if ((m & 7) == 6) asm volatile("" ::: "memory");   // bound the twiddle loads in flight
+            for (int m = 0; m < 16; ++m) xw[17 * m] = v[16 * r + m];
+        } else {
+            if constexpr (SYNC0) __syncthreads();
+            float4 w2s[8];
+#pragma unroll
+            for (int mp = 0; mp < 8; ++mp) w2s[mp] = lds128_nohoist(tw4 + ((16 * r) >> 1) + mp);
+#pragma unroll
+            for (int m = 0; m < 16; m += 2) {
+                const float4 w2 = w2s[m >> 1];
+                xw[17 * m] = (r || m) ? cmw(v[16 * r + m], make_float2(w2.x, w2.y)) : v[16 * r];
+                xw[17 * (m + 1)] = cmw(v[16 * r + m + 1], make_float2(w2.z, w2.w));
+            }
+            asm volatile("" ::: "memory");
         }
         if (r == 0) before_sync();
+        bar_pre(r);
         mark(12);
         __syncthreads();
+        bar_post(r);
         if (r == 0) mid();   // every thread's stage-1 inputs of this tile have been consumed
         mark(13);
         float2 y[16];
@@ -366,13 +404,20 @@ __device__ __forceinline__ void dft_tile_db(float2* v, const float2* tw, float2*
 // EARLY (D = 512): the first half of the next tile's inputs is loaded after the first exchange
 // round (its registers v[0..15] are dead then), the second half after the last round -- half
 // a tile more time in flight than loading both halves at the end.
-template <int D, int MINB, bool FULLPF = (MINB <= 3), bool REAL = false, bool EARLY = false>
-__global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
+// CST: the B tiles' coefficients go to global memory by TMA stores: each exchange round's
+// 8 columns x 256 rows are written (times E(n)) into one half of the F buffer -- idle in B
+// jobs -- as a box [m div R1][m mod R1][column] and stored by one cp.async.bulk.tensor (16 KB)
+// that thread 0 issues after the next barrier; before a half is rewritten thread 0 waits for
+// the earlier stores' shared-memory reads.  Whole-box stores replace the per-thread 8-byte
+// stores that touched 64 bytes of each of four lines per warp instruction.
+template <int D, int MINB, bool FULLPF = (MINB <= 3), bool REAL = false, bool EARLY = false, bool CST = false>
+__global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_constant__ CUtensorMap cmap) {
     using K = Cfg<D>;
     constexpr int R1 = K::R1, Q = K::Q, M = D, AC = K::ACOL, BT = K::BT;
     constexpr int N = Q * D;       // N = L / a = q d here (the host checks)
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2* X2 = reinterpret_cast<float2*>(smem_raw);
+    static_assert(!CST || (D == 512 && K::FE >= 2 * 2048), "F buffer holds two 16 KB store boxes (D = 512)");
+    extern __shared__ __align__(128) unsigned char smem_tma[];
+    float2* X2 = reinterpret_cast<float2*>(smem_tma);
     float2* F = X2 + K::XE;        // F[col * FS + nu], col < ACOL
     float2* twt = F + K::FE;       // twt[t][m] = W_D^{t m}
     __shared__ int jobsm[2];       // next job, 1 if its first tile's inputs were prefetched
@@ -477,7 +522,19 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
             pend = nullptr;
         }
     };
+    // CST (thread 0): the store box written by the last exchange round, issued after the next
+    // barrier -- kept in shared memory (thread 0 alone uses it; registers are at the cap)
+    __shared__ int cst_box[5];   // pending, half, x, y, z
+    auto cst_issue = [&]() {
+        if (CST && cst_box[0]) {
+            tma::store_3d(&cmap, F + cst_box[1] * 2048, cst_box[2], cst_box[3], cst_box[4]);
+            tma::bulk_commit();
+            cst_box[0] = 0;
+        }
+    };
     if (tid == 0) {
+        cst_box[0] = 0;
+        if (CST && (tma::saddr(F) & 127)) __trap();   // TMA boxes are 128-byte aligned
         jobsm[0] = atomicAdd(queue, 1);
         jobsm[1] = 0;
     }
@@ -497,6 +554,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
         }
         mark(1);
         __syncthreads();
+        if (CST && tid == 0) cst_issue();   // the previous job's last box
         mark(3);
         const int isA = jobdec[0];
         if (isA < 0) break;
@@ -535,7 +593,13 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
             // ---------------- pass A: columns j0 .. j0 + 7 ----------------
             const int j0 = idx * AC;
             // Zak DFT of 8 columns: F_j(nu), nu = 16 r + i + R1 m2, stored at F[col * FS + nu]
-            dft_tile<D>(pre, tw, X2, s8, h8, s8, h8, [&] { if (tid == 0) flush(); },
+            dft_tile<D>(pre, tw, X2, s8, h8, s8, h8,
+                        [&] {
+                            if (tid == 0) {
+                                flush();
+                                if (CST) tma::bulk_wait_read0();   // F is rewritten below
+                            }
+                        },
                         [&] {
                             if (!EARLY) load_g(j0, 0, 0);
                             if ((FULLPF || EARLY) && R1 > 16) load_g(j0, 0, 1);
@@ -579,7 +643,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                     for (int k = 16; k < R1; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
                 }
                 mark(22);
-                __syncthreads();   // previous tile's readers are done with X
+                // (the barrier for the previous tile's readers of X is inside the tile: SYNC0)
                 // ring layout ws[slot][j][n' >> 2][n' & 3][kappa]: one 128-byte line per
                 // (j, n' >> 2), holding columns n = 4 n' + kappa in natural order.  A warp of
                 // role M3 holds the 4 kappa of one column x 8 consecutive n': every store
@@ -588,7 +652,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                 const int kap = ((jM / A.c - uM) % Q + Q) % Q;
                 // n' = 16 r + iM + R1 m2: line n' >> 2 = 4 r + (R1 / 4) m2 + (iM >> 2), position 4 (iM & 3) + kappa
                 float2* dst = wsl + (int64_t)jM * (Q * D) + (iM >> 2) * 16 + (iM & 3) * 4 + kap;
-                dft_tile<D>(pre, tw, X2, s8, h8, 4 * colM + uM, iM,
+                dft_tile<D, true>(pre, tw, X2, s8, h8, 4 * colM + uM, iM,
                             [&] { if (h == 3 && tid == 0) claim_ready(); },
                             [&] {
                                 if (h < 3) {
@@ -619,11 +683,9 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                 const int n = idx * 16 + 8 * bt + s8;
                 const float2 e = ldg_na2(A.E + n);   // issued here (volatile), used at the emit
                 float2* dst = A.out + (int64_t)w * M * N + n;
-                if (bt) {
-                    if (!FULLPF && R1 > 16) load_ring(w, idx, bt, 1);   // second half (the first was prefetched)
-                    __syncthreads();   // previous tile's readers are done with X
-                }
-                dft_tile<D>(pre, tw, X2, s8, h8, s8, h8,
+                if (bt && !FULLPF && R1 > 16) load_ring(w, idx, bt, 1);   // second half (the first was prefetched)
+                // (the barrier for the previous tile's readers of X is inside the tile: SYNC0)
+                dft_tile<D, true>(pre, tw, X2, s8, h8, s8, h8,
                             [&] {
                                 if (tid == 0) {
                                     flush();
@@ -639,11 +701,25 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                                 }
                             },
                             [&](int r, const float2* y) {
-                                if (A.dbg & (4 | 64)) return;
+                                if constexpr (CST) {   // (D = 512: round r writes half r)
+                                    float2* Fh = F + r * 2048;
 #pragma unroll
-                                for (int m2 = 0; m2 < 16; ++m2) {
-                                    const int m = 16 * r + h8 + R1 * m2;
-                                    __stcs(dst + m * N, cmw(y[m2], e));
+                                    for (int m2 = 0; m2 < 16; ++m2) Fh[(m2 * 16 + h8) * 8 + s8] = cmw(y[m2], e);
+                                    tma::fence_proxy_async_smem();
+                                    if (tid == 0) {
+                                        cst_box[0] = 1;
+                                        cst_box[1] = r;
+                                        cst_box[2] = idx * 16 + 8 * bt;
+                                        cst_box[3] = 16 * r;
+                                        cst_box[4] = w * (M / R1);
+                                    }
+                                } else {
+                                    if (A.dbg & (4 | 64)) return;
+#pragma unroll
+                                    for (int m2 = 0; m2 < 16; ++m2) {
+                                        const int m = 16 * r + h8 + R1 * m2;
+                                        __stcs(dst + m * N, cmw(y[m2], e));
+                                    }
                                 }
                             }, A.dbg, mark, NoMid(),
                             [&] {
@@ -651,6 +727,12 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
                                     if (bt + 1 < BT) load_ring(w, idx, bt + 1, 0);
                                     else prefetch_next0();
                                 }
+                            },
+                            [&](int) {   // the half this round's emit writes is read by no store
+                                if (CST && tid == 0) tma::bulk_wait_read0();
+                            },
+                            [&](int) {   // every thread's box of the previous round is written
+                                if (CST && tid == 0) cst_issue();
                             });
             }
             // The ring lines this job read are dead (this job is their only reader; the
@@ -663,7 +745,13 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A) {
         }
     }
     __syncthreads();   // the last job's stores are ordered before its completion signal
-    if (tid == 0) flush();
+    if (tid == 0) {
+        flush();
+        if (CST) {
+            cst_issue();
+            tma::bulk_wait0();
+        }
+    }
 }
 
 // ------------------------------------------------------------------------------------
