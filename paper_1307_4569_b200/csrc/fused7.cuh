@@ -202,6 +202,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// completion signal: a release reduction (after a CTA barrier it orders every thread's earlier
+// stores / discards of the job before the count, like CUTLASS's semaphore arrive) -- no full fence
+__device__ __forceinline__ void signal_release(int* p) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void spin_until(const int* p, int target) {
     if (ld_acquire(p) >= target) return;
     while (ld_acquire(p) < target) __nanosleep(64);
@@ -517,8 +522,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
     int* pend = nullptr;
     auto flush = [&]() {
         if (pend) {
-            __threadfence();
-            atomicAdd(pend, 1);
+            signal_release(pend);
             pend = nullptr;
         }
     };
@@ -857,8 +861,7 @@ __global__ void __launch_bounds__(128, MINB) fused7t_kernel(Args A, const __grid
     int* pend = nullptr;
     auto flush = [&]() {
         if (pend) {
-            __threadfence();
-            atomicAdd(pend, 1);
+            signal_release(pend);
             pend = nullptr;
         }
     };

@@ -69,8 +69,7 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
         __syncthreads();
         if (tid == 0) {
             if (pend) {
-                __threadfence();
-                atomicAdd(pend, 1);
+                signal_release(pend);
                 pend = nullptr;
             }
             jobsm = atomicAdd(queue, 1);
@@ -200,8 +199,7 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
     }
     __syncthreads();
     if (tid == 0 && pend) {
-        __threadfence();
-        atomicAdd(pend, 1);
+        signal_release(pend);
     }
 }
 

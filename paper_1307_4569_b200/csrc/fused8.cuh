@@ -177,8 +177,7 @@ __global__ void __launch_bounds__(256, MINB) fused8_kernel(Args A) {
     int* pend = nullptr;
     auto flush = [&]() {
         if (pend) {
-            __threadfence();
-            atomicAdd(pend, 1);
+            v7::signal_release(pend);
             pend = nullptr;
         }
     };
