@@ -1,6 +1,6 @@
 set -x
-timeout 600 python -m pytest tests/test_gpu_fused7.py tests/test_gpu_inverse.py -x -q > gpurun_out/t_it.log 2>&1; echo rc=$? >> gpurun_out/t_it.log
-CFG=5 ENVS="NSDGT_FUSED=7;NSDGT_FUSED=7;NSDGT_CTAS=4" timeout 300 python tools/v7env.py > gpurun_out/env5.log 2>&1
-CFG=3 WT=256 ENVS="NSDGT_FUSED=7;NSDGT_FUSED=7" timeout 300 python tools/v7env.py > gpurun_out/env3.log 2>&1
-timeout 200 python bench.py --steps 5 --inverse --no-e2e --no-cpu-baseline > gpurun_out/inv5.json 2>/dev/null
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/t_all.log 2>&1; echo rc=$? >> gpurun_out/t_all.log
+timeout 300 python bench.py --config 1 --steps 20 --no-cpu-baseline > gpurun_out/b1.json 2>gpurun_out/b1.err
+NSDGT_TINY=0 timeout 300 python bench.py --config 1 --steps 20 --no-cpu-baseline > gpurun_out/b1_old.json 2>>gpurun_out/b1.err
+timeout 300 python bench.py --config 1 --steps 20 --inverse --no-cpu-baseline > gpurun_out/b1_inv.json 2>>gpurun_out/b1.err
 echo done
