@@ -7,7 +7,8 @@ g_{n,k} = M_{sn+bk} T_{an} g (Prop. lattNF), the frame operato
 S = sum <f, pi(lam) g> pi(lam) g (Eq. frameop) and the inversion
 formula with the canonical dual S^{-1} g.  Phases here are
 computed in floating point from the L-periodic definitions (independent of the
-oracle's exact integer reduction).
+oracle's exact integer reduction).  The dense frame operator, canonical dual and tight
+windows live in one place, oracle/windows.py (pinned in test_oracle_pins.py).
 """
 from __future__ import annotations
 
@@ -57,23 +58,6 @@ def dense_dgt(f, g, a, M, lam1, lam2) -> np.ndarray:
     L = len(g)
     G = synthesis_matrix(g, a, M, lam1, lam2)
     return (G.conj().T @ np.asarray(f, dtype=np.complex128)).reshape(M, L // a)
-
-
-def frame_operator(g, a, M, lam1, lam2) -> np.ndarray:
-    G = synthesis_matrix(g, a, M, lam1, lam2)
-    return G @ G.conj().T
-
-
-def canonical_dual(g, a, M, lam1, lam2) -> np.ndarray:
-    S = frame_operator(g, a, M, lam1, lam2)
-    return np.linalg.solve(S, np.asarray(g, dtype=np.complex128))
-
-
-def canonical_tight(g, a, M, lam1, lam2) -> np.ndarray:
-    S = frame_operator(g, a, M, lam1, lam2)
-    ev, V = np.linalg.eigh(S)
-    Sm12 = (V * (1.0 / np.sqrt(ev))) @ V.conj().T
-    return Sm12 @ np.asarray(g, dtype=np.complex128)
 
 
 def synthesize(c: np.ndarray, gamma, a, M, lam1, lam2) -> np.ndarray:

@@ -85,8 +85,8 @@ def test_round_trip_with_dual_window(torch_cuda, nsdgt, oracle_mod, k):
     pf = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, real_input=np.isrealobj(f))
     c = pf.execute(torch.from_numpy(f).cuda())
     if k == 1:
-        import dense
-        gamma = dense.canonical_dual(g, wl.a, wl.M, wl.lam1, wl.lam2)
+        import oracle
+        gamma = oracle.windows.canonical_dual(g, wl.a, wl.M, wl.lam1, wl.lam2)
         pi = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, gamma, dtype=wl.dtype)
         fr = pi.inverse(c).cpu().numpy()
         assert rel(fr, f.astype(complex)) <= 1e-10

@@ -135,7 +135,7 @@ def test_energy_tight(oracle_mod, L, a, M, l1, l2):
     """P8: for the canonical tight window g_t = S^{-1/2} g, ||c||^2 = ||f||^2, and for
     any scaling t*g_t: ||c||^2 = (M N / L) ||t g_t||^2 ||f||^2."""
     g = pgauss(L, a * M / L)
-    gt = dense.canonical_tight(g, a, M, l1, l2)
+    gt = oracle_mod.windows.canonical_tight(g, a, M, l1, l2)
     f, _ = random_pair(L, 18)
     c = oracle_mod.dgt(f, gt, a, M, l1, l2)
     assert abs(np.vdot(c, c).real - np.vdot(f, f).real) < 1e-11 * np.vdot(f, f).real
@@ -153,7 +153,7 @@ def test_perfect_reconstruction(oracle_mod, L, a, M, l1, l2):
     """P9: f = sum c(m,n) M_{b(m+w(n))} T_{an} gamma with gamma = S^{-1} g.
     Includes config 1 itself (L=240, a=8, M=12, quincunx, pgauss with tfr = aM/L)."""
     g = pgauss(L, a * M / L)
-    gamma = dense.canonical_dual(g, a, M, l1, l2)
+    gamma = oracle_mod.windows.canonical_dual(g, a, M, l1, l2)
     f, _ = random_pair(L, 19)
     c = oracle_mod.dgt(f, g, a, M, l1, l2)
     f_rec = dense.synthesize(c, gamma, a, M, l1, l2)
@@ -232,7 +232,7 @@ def test_idgt_perfect_reconstruction(oracle_mod, L, a, M, l1, l2):
     """idgt(dgt(f, g), S^{-1} g) = f (inversion formula), the dual from the
     dense frame operator."""
     g = pgauss(L, a * M / L)
-    gamma = dense.canonical_dual(g, a, M, l1, l2)
+    gamma = oracle_mod.windows.canonical_dual(g, a, M, l1, l2)
     f, _ = random_pair(L, 34)
     f_rec = oracle_mod.idgt(oracle_mod.dgt(f, g, a, M, l1, l2), gamma, a, M, l1, l2)
     assert rel(f_rec, f.astype(complex)) < 1e-11
