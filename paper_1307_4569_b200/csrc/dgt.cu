@@ -27,6 +27,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/nsdgt.h"
 #include "cplx.cuh"
 #include "fft_smem.cuh"
@@ -1998,6 +2000,15 @@ static int execute(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) 
 
 using namespace nsdgt;
 
+namespace {
+// NVTX range around every C-ABI entry point (SURVEY §5 tracing): header-only nvtx3, a no-op
+// unless a tool (nsys, ncu --nvtx) is attached
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 extern "C" {
 
 const char* dgt_version(void) { return "nsdgt 0.1 (sm_100a)"; }
@@ -2076,11 +2087,13 @@ static int make_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l
 
 int dgt_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int dtype,
              int flags, int64_t max_chunk, int force_shear, int64_t s0, int64_t s1, void* cuda_stream) {
+    NvtxRange nvtx_range("dgt_plan");
     return make_plan(out, L, a, M, l1, l2, g, dtype, flags, max_chunk, force_shear, s0, s1, cuda_stream, true);
 }
 
 int dgt_plan_fir(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g, int64_t Lg,
                  int64_t Lb, int dtype, int flags, void* cuda_stream) {
+    NvtxRange nvtx_range("dgt_plan_fir");
     if (!out || !g) return fail(DGT_EINVAL, "null pointer");
     *out = nullptr;
     if (dtype != DGT_C64 && dtype != DGT_C128) return fail(DGT_EINVAL, "bad dtype");
@@ -2176,6 +2189,7 @@ int dgt_plan_fir(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, i
 
 int dgt_plan_multiwindow(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l1, int64_t l2, const void* g,
                          int dtype, int flags, void* cuda_stream) {
+    NvtxRange nvtx_range("dgt_plan_multiwindow");
     if (!out || !g) return fail(DGT_EINVAL, "null pointer");
     *out = nullptr;
     if (dtype != DGT_C64 && dtype != DGT_C128) return fail(DGT_EINVAL, "bad dtype");
@@ -2257,6 +2271,7 @@ int dgt_plan_multiwindow(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64
 }
 
 int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_stream) {
+    NvtxRange nvtx_range("dgt_execute");
     Plan* P = (Plan*)plan;
     if (!P) return fail(DGT_EINVAL, "null plan");
     if (W < 0) return fail(DGT_EINVAL, "W < 0");
@@ -2271,6 +2286,7 @@ int dgt_execute(dgt_plan_t plan, const void* f, void* c, int64_t W, void* cuda_s
 }
 
 int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void* cuda_stream) {
+    NvtxRange nvtx_range("dgt_execute_inverse");
     Plan* P = (Plan*)plan;
     if (!P) return fail(DGT_EINVAL, "null plan");
     if (P->ola) return fail(DGT_EUNSUPPORTED, "synthesis is not implemented for shear-OLA plans");
@@ -2286,6 +2302,7 @@ int dgt_execute_inverse(dgt_plan_t plan, const void* c, void* f, int64_t W, void
 }
 
 int dgt_window_dual(dgt_plan_t plan, int kind, void* out, int flags, void* cuda_stream) {
+    NvtxRange nvtx_range("dgt_window_dual");
     Plan* P = (Plan*)plan;
     if (!P || !out) return fail(DGT_EINVAL, "null pointer");
     if (P->ola) return fail(DGT_EUNSUPPORTED, "dual windows are not implemented for shear-OLA plans");
@@ -2374,6 +2391,7 @@ static int alloc_host_staging(Plan* P) {
 }
 
 int dgt_execute_host(dgt_plan_t plan, const void* f_host, void* c_host, int64_t W, void* cuda_stream) {
+    NvtxRange nvtx_range("dgt_execute_host");
     Plan* P = (Plan*)plan;
     if (!P) return fail(DGT_EINVAL, "null plan");
     if (W < 0) return fail(DGT_EINVAL, "W < 0");
