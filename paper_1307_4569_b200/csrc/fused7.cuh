@@ -187,7 +187,7 @@ struct Args {
     unsigned long long* log;   // dbg & 16: per-CTA phase timestamps (CTAs < 8, 4096 entries each)
     int dbg;             // experiment knobs (0 in production; results are wrong with all but 16):
                          // 1 no dependency spin, 4 no global stores, 8 no DFT arithmetic,
-                         // 16 phase trace (-DNSDGT_TRACE builds), 32 no G' loads,
+                         // 16 phase trace (-DNSDGT_TRACE builds), 32 no G' loads (fused8 only),
                          // 64 no c stores, 128 no ring stores, 256 skip B jobs, 512 skip A jobs
 };
 
@@ -425,8 +425,8 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
     float2* X2 = reinterpret_cast<float2*>(smem_tma);
     float2* F = X2 + K::XE;        // F[col * FS + nu], col < ACOL
     float2* twt = F + K::FE;       // twt[t][m] = W_D^{t m}
-    __shared__ int jobsm[2];       // next job, 1 if its first tile's inputs were prefetched
-    __shared__ int jobdec[4];      // decoded current job: isA (or -1 = done), w, idx
+    __shared__ int jobsm[6];       // next job, 1 if its first tile's inputs were prefetched, its isA, w, idx, slot
+    __shared__ int jobdec[6];      // decoded current job: isA (or -1 = done), w, idx, gen, slot
     const int tid = threadIdx.x;
     // thread-role maps (t = stage-1 lane, i = stage-2 lane):
     //   S1 / M1 (Zak tile, B tiles, stage 1 of product tiles): slot s8 = tid & 7, t / i = h8 = tid >> 3
@@ -474,46 +474,48 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
         const float4* G4 = A.Gp + ((int64_t)((j0 / AC) * 4 + h) * (R1 / 2)) * 128 + h8 * 8 + s8;
 #pragma unroll
         for (int kp = 8 * b; kp < 8 * b + 8 && kp < R1 / 2; ++kp) {
-            const float4 g = (A.dbg & 32) ? make_float4(1.f, 0.f, 1.f, 0.f) : ldg_na(G4 + kp * 128);
+            const float4 g = ldg_na(G4 + kp * 128);
             pre[2 * kp] = make_float2(g.x, g.y);
             pre[2 * kp + 1] = make_float2(g.z, g.w);
         }
     };
     // pass-B input: ring line (j, line) holds columns n = 16 line + p at position p; tile bt
     // reads positions 8 bt + s8
-    auto load_ring = [&](int w, int line, int bt, int b) {
-        const float2* src = A.ws + (int64_t)(w % A.S) * MQD + (int64_t)h8 * (Q * D) + line * 16 + 8 * bt + s8;   // (w % S: rare path)
+    auto load_ring = [&](int slot, int line, int bt, int b) {   // slot = w mod S
+        const float2* src = A.ws + (int64_t)slot * MQD + (int64_t)h8 * (Q * D) + line * 16 + 8 * bt + s8;
 #pragma unroll
         for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ld_cg(src + (int64_t)(16 * k) * (Q * D));
     };
-    auto load_first = [&](int isA, int w, int idx, int b) {   // first tile of a job, half b
+    auto load_first = [&](int isA, int w, int idx, int slot, int b) {   // first tile of a job, half b
         if (isA) load_f(w, idx * AC, b);
-        else load_ring(w, idx, 0, b);
+        else load_ring(slot, idx, 0, b);
     };
     int pnext = -1;
     // Cross-job prefetch.  claim_ready (thread 0, before the last tile's exchange barrier)
     // publishes the next job and whether its inputs may be read now (A: always -- f is
     // read-only; B: its dependency already holds).  prefetch_next (every thread, after that
     // barrier, when pre[] is dead) loads the first half behind the tile's stage 2.
+    // (thread 0 decodes the next job once and publishes it: the integer divisions of decode
+    // stay out of the 128 threads' prefetch path)
     auto claim_ready = [&]() {
-        int isA0, idx0, w0, ready = 0;
+        int isA0, idx0, w0, ready = 0, slot0 = 0;
         if (decode(pnext, A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
-            const int gen0 = w0 / A.S, slot0 = w0 - gen0 * A.S;
+            const int gen0 = w0 / A.S;
+            slot0 = w0 - gen0 * A.S;
             ready = isA0 || (A.dbg & 1) || ld_acquire(doneA + slot0) >= (gen0 + 1) * A.nA;
+            jobsm[2] = isA0; jobsm[3] = w0; jobsm[4] = idx0; jobsm[5] = slot0;
         }
         jobsm[0] = pnext;
         jobsm[1] = ready;
     };
     auto prefetch_next = [&]() {
-        int isA0, idx0, w0;
-        if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
-            if (!EARLY) load_first(isA0, w0, idx0, 0);
-            if ((FULLPF || EARLY) && R1 > 16) load_first(isA0, w0, idx0, 1);
+        if (jobsm[1]) {
+            if (!EARLY) load_first(jobsm[2], jobsm[3], jobsm[4], jobsm[5], 0);
+            if ((FULLPF || EARLY) && R1 > 16) load_first(jobsm[2], jobsm[3], jobsm[4], jobsm[5], 1);
         }
     };
     auto prefetch_next0 = [&]() {   // EARLY: the first half
-        int isA0, idx0, w0;
-        if (jobsm[1] && decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) load_first(isA0, w0, idx0, 0);
+        if (jobsm[1]) load_first(jobsm[2], jobsm[3], jobsm[4], jobsm[5], 0);
     };
     // Completion signals are deferred: thread 0 publishes "job done" (fence + counter add)
     // once it is into its next job's first tile, when the job's stores have drained and
@@ -551,7 +553,8 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
         if (tid == 0) {
             int isA0, idx0, w0;
             if (decode(jobsm[0], A.W, A.lag, A.nA, A.nB, &isA0, &w0, &idx0)) {
-                jobdec[0] = isA0; jobdec[1] = w0; jobdec[2] = idx0;
+                const int gen0 = w0 / A.S;
+                jobdec[0] = isA0; jobdec[1] = w0; jobdec[2] = idx0; jobdec[3] = gen0; jobdec[4] = w0 - gen0 * A.S;
             } else {
                 jobdec[0] = -1;
             }
@@ -563,7 +566,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
         const int isA = jobdec[0];
         if (isA < 0) break;
         const int w = jobdec[1], idx = jobdec[2];
-        const int gen = w / A.S, slot = w - gen * A.S;
+        const int gen = jobdec[3], slot = jobdec[4];
         float2* wsl = A.ws + (int64_t)slot * MQD;
         if (tid == 0 && !(A.dbg & 1)) {
             const int* cnt = isA ? doneB + slot : (pref ? nullptr : doneA + slot);
@@ -589,9 +592,9 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
         }
         if (!pref) {
             if (!isA) __syncthreads();
-            load_first(isA, w, idx, 0);
+            load_first(isA, w, idx, slot, 0);
         }
-        if (R1 > 16 && (!FULLPF || !pref)) load_first(isA, w, idx, 1);
+        if (R1 > 16 && (!FULLPF || !pref)) load_first(isA, w, idx, slot, 1);
         mark(pref ? 6 : 5);
         if (isA) {
             // ---------------- pass A: columns j0 .. j0 + 7 ----------------
@@ -621,11 +624,12 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
             // four product tiles: tile h = columns j0 + 2h, j0 + 2h + 1, slot s -> (col = s >> 2, u = s & 3)
             const int wq = tid >> 5, ln = tid & 31;
             const int colM = wq >> 1, uM = ln >> 3, iM = (ln & 7) + 8 * (wq & 1);   // role M3
+            const int kap = (j0 / A.c - uM) & (Q - 1);   // kappa = (l - u) mod q: l is the job's (c % 8 == 0)
 #pragma unroll 1
             for (int h = 0; h < 4; ++h) {
                 const int fcol = 2 * h + (s8 >> 2);   // F column of this stage-1 slot
                 const int jS = j0 + fcol;
-                const int sig = (int)((((int64_t)jS * A.beta - ((int64_t)A.Kmod * jS) % D) % D + D) % D);
+                const int sig = (jS * (A.beta - A.Kmod)) & (D - 1);   // (j beta - K j) mod D, D a power of 2
                 // the next job is claimed in the last tile: claiming it earlier (at this job's
                 // start or one tile earlier) measured 50 % / 1.3 % slower -- the later claim
                 // keeps B jobs behind their A jobs
@@ -653,7 +657,6 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
                 // role M3 holds the 4 kappa of one column x 8 consecutive n': every store
                 // fills 2 whole lines.
                 const int jM = j0 + 2 * h + colM;
-                const int kap = ((jM / A.c - uM) % Q + Q) % Q;
                 // n' = 16 r + iM + R1 m2: line n' >> 2 = 4 r + (R1 / 4) m2 + (iM >> 2), position 4 (iM & 3) + kappa
                 float2* dst = wsl + (int64_t)jM * (Q * D) + (iM >> 2) * 16 + (iM & 3) * 4 + kap;
                 dft_tile<D, true>(pre, tw, X2, s8, h8, 4 * colM + uM, iM,
@@ -687,7 +690,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
                 const int n = idx * 16 + 8 * bt + s8;
                 const float2 e = ldg_na2(A.E + n);   // issued here (volatile), used at the emit
                 float2* dst = A.out + (int64_t)w * M * N + n;
-                if (bt && !FULLPF && R1 > 16) load_ring(w, idx, bt, 1);   // second half (the first was prefetched)
+                if (bt && !FULLPF && R1 > 16) load_ring(slot, idx, bt, 1);   // second half (the first was prefetched)
                 // (the barrier for the previous tile's readers of X is inside the tile: SYNC0)
                 dft_tile<D, true>(pre, tw, X2, s8, h8, s8, h8,
                             [&] {
@@ -698,8 +701,8 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
                             },
                             [&] {
                                 if (bt + 1 < BT) {
-                                    if (!EARLY) load_ring(w, idx, bt + 1, 0);
-                                    if ((FULLPF || EARLY) && R1 > 16) load_ring(w, idx, bt + 1, 1);
+                                    if (!EARLY) load_ring(slot, idx, bt + 1, 0);
+                                    if ((FULLPF || EARLY) && R1 > 16) load_ring(slot, idx, bt + 1, 1);
                                 } else {
                                     prefetch_next();
                                 }
@@ -728,7 +731,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
                             }, A.dbg, mark, NoMid(),
                             [&] {
                                 if (EARLY) {
-                                    if (bt + 1 < BT) load_ring(w, idx, bt + 1, 0);
+                                    if (bt + 1 < BT) load_ring(slot, idx, bt + 1, 0);
                                     else prefetch_next0();
                                 }
                             },
