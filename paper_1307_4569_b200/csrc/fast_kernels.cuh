@@ -330,6 +330,7 @@ int launch_fast(FastPlan* fp, const void* f, int real_in, void* ws, void* c, int
     a.f = (const float2*)f; a.out = (float2*)c; a.ws = (float2*)ws; a.Gp = (const float4*)fp->Gp;
     a.E = (const float2*)fp->E; a.ctr = fp->counters; a.W = (int)W; a.N = fp->N; a.c = fp->c; a.Kmod = fp->Kmod;
     a.beta = fp->beta; a.S = fp->S; a.lag = fp->lag; a.nA = fp->nA; a.nB = fp->nB;
+    a.sig0 = ((fp->beta - fp->Kmod) & (fp->D - 1)) == 0 ? 1 : 0;
     a.dbg = fp->dbg;
     if (fp->tracelog) {
         cudaMemsetAsync(fp->tracelog, 0, sizeof(unsigned long long) * 8 * 4096, st);

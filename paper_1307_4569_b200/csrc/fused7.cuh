@@ -184,6 +184,7 @@ struct Args {
     int* ctr;            // [0] job queue, [1..S] doneA per slot, [1+S..2S] doneB per slot
     int W, N, c, Kmod, beta;
     int S, lag, nA, nB;
+    int sig0;            // sigma_j = 0 for every column j (the plan checks): wrap-free F gathers
     unsigned long long* log;   // dbg & 16: per-CTA phase timestamps (CTAs < 8, 4096 entries each)
     int dbg;             // experiment knobs (0 in production; results are wrong with all but 16):
                          // 1 no dependency spin, 4 no global stores, 8 no DFT arithmetic,
@@ -616,6 +617,8 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
                             for (int m2 = 0; m2 < 16; ++m2) {
                                 F[s8 * K::FS + 16 * r + h8 + R1 * m2] = y[m2];
                             }
+                            // F(D) = F(0): the sigma = 0 gathers below read F(D - t - 16 k) without a wrap
+                            if (r == 0 && h8 == 0) F[s8 * K::FS + D] = y[0];
                         }, A.dbg, mark, NoMid(),
                         [&] { if (EARLY) load_g(j0, 0, 0); });
             mark(20);
@@ -639,16 +642,32 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
                 // F index (sigma - t - 16 k) mod D = (e0 - 16 k) mod D, e0 = (sigma - t) mod D: the
                 // first (e0 >> 4) + 1 values need no wrap
                 const float2* Fc = F + fcol * K::FS;
-                const int e0 = (sig - h8) & (D - 1);
+                if (A.sig0) {
+                    // sigma_j = 0 for every column (configs 3 and 5): F((-t - 16 k) mod D) is
+                    // F(D - t - 16 k) in [1, D] (F(D) duplicates F(0)): constant offsets
+                    const float2* Fb = Fc + (D - h8);
 #pragma unroll
-                for (int k = 0; k < 16; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
-                if (R1 > 16) {
-                    if (!FULLPF) {
-                        asm volatile("" ::: "memory");
-                        load_g(j0, h, 1);
+                    for (int k = 0; k < 16; ++k) pre[k] = cmw(Fb[-16 * k], pre[k]);
+                    if (R1 > 16) {
+                        if (!FULLPF) {
+                            asm volatile("" ::: "memory");
+                            load_g(j0, h, 1);
+                        }
+#pragma unroll
+                        for (int k = 16; k < R1; ++k) pre[k] = cmw(Fb[-16 * k], pre[k]);
                     }
+                } else {
+                    const int e0 = (sig - h8) & (D - 1);
 #pragma unroll
-                    for (int k = 16; k < R1; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
+                    for (int k = 0; k < 16; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
+                    if (R1 > 16) {
+                        if (!FULLPF) {
+                            asm volatile("" ::: "memory");
+                            load_g(j0, h, 1);
+                        }
+#pragma unroll
+                        for (int k = 16; k < R1; ++k) pre[k] = cmw(Fc[(e0 - 16 * k) & (D - 1)], pre[k]);
+                    }
                 }
                 mark(22);
                 // (the barrier for the previous tile's readers of X is inside the tile: SYNC0)
