@@ -466,7 +466,11 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
         } else {
             const float2* fw = A.f + (int64_t)w * M * D + j0 + s8;
 #pragma unroll
+#ifdef NSDGT_XP_NOFR   // experiment builds only: no f / ring loads (results wrong)
+            for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = make_float2((float)k, (float)(j0 + w));
+#else
             for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ldg_na2(fw + (int64_t)(h8 + 16 * k) * M);
+#endif
         }
     };
     // G' of product tile h (slot s8 = 4 col + u, lane t).  Layout [j0 / 8][h][kp][t][slot] of
@@ -475,7 +479,11 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
         const float4* G4 = A.Gp + ((int64_t)((j0 / AC) * 4 + h) * (R1 / 2)) * 128 + h8 * 8 + s8;
 #pragma unroll
         for (int kp = 8 * b; kp < 8 * b + 8 && kp < R1 / 2; ++kp) {
+#ifdef NSDGT_XP_NOG   // experiment builds only: no G' loads
+            const float4 g = make_float4((float)kp, 1.f, (float)h, 0.5f);
+#else
             const float4 g = ldg_na(G4 + kp * 128);
+#endif
             pre[2 * kp] = make_float2(g.x, g.y);
             pre[2 * kp + 1] = make_float2(g.z, g.w);
         }
@@ -485,7 +493,11 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
     auto load_ring = [&](int slot, int line, int bt, int b) {   // slot = w mod S
         const float2* src = A.ws + (int64_t)slot * MQD + (int64_t)h8 * (Q * D) + line * 16 + 8 * bt + s8;
 #pragma unroll
+#ifdef NSDGT_XP_NOFR
+        for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = make_float2((float)k, (float)(line + slot));
+#else
         for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ld_cg(src + (int64_t)(16 * k) * (Q * D));
+#endif
     };
     auto load_first = [&](int isA, int w, int idx, int slot, int b) {   // first tile of a job, half b
         if (isA) load_f(w, idx * AC, b);
