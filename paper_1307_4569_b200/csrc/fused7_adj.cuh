@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
     float2* F = X2 + K::XE;        // Fc[col * FS + nu], col < ACOL
     float2* twt = F + K::FE;
     __shared__ int jobsm;
+    __shared__ int jobdec[6];   // decoded job (thread 0): ok, isB, w, idx, gen, slot
     const int tid = threadIdx.x;
     const int s8 = tid & 7, h8 = tid >> 3;                  // roles S1 / M1
     const int wq = tid >> 5, ln = tid & 31;                 // role M3 (product tiles, stage 2)
@@ -73,11 +74,15 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
                 pend = nullptr;
             }
             jobsm = atomicAdd(queue, 1);
+            int isB0, w0, idx0;
+            jobdec[0] = decode(jobsm, A.W, A.lag, A.nB, A.nA, &isB0, &w0, &idx0) ? 1 : 0;
+            const int gen0 = w0 / A.S;
+            jobdec[1] = isB0; jobdec[2] = w0; jobdec[3] = idx0; jobdec[4] = gen0; jobdec[5] = w0 - gen0 * A.S;
         }
         __syncthreads();
-        int isB, w, idx;
-        if (!decode(jobsm, A.W, A.lag, A.nB, A.nA, &isB, &w, &idx)) break;
-        const int gen = w / A.S, slot = w - gen * A.S;
+        if (!jobdec[0]) break;
+        const int isB = jobdec[1], w = jobdec[2], idx = jobdec[3];
+        const int gen = jobdec[4], slot = jobdec[5];
         float2* wsl = A.ws + (int64_t)slot * MN;
         // B' reads only the (read-only) coefficients; its dependency gates the ring stores, so
         // its first tile's loads are issued before the wait and overlap it
@@ -120,11 +125,12 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
         } else {
             // ---------------- pass A': columns j0 .. j0 + 7 ----------------
             const int j0 = idx * AC;
+            const int lJ = j0 / A.c;   // l of every column of the job (c % 8 == 0)
             // product tile h's input: stage-1 slot s8 = (column j0 + 2h + (s8 >> 2), u = s8 & 3),
             // lane t = h8: ws'[j][kappa + q (t + 16 k)] (conjugated when used)
             auto load_r = [&](int h) {
                 const int jS = j0 + 2 * h + (s8 >> 2);
-                const int kapS = ((jS / A.c - (s8 & 3)) % Q + Q) % Q;
+                const int kapS = (lJ - (s8 & 3)) & (Q - 1);
                 const float2* src = wsl + (int64_t)jS * N + kapS + 4 * h8;
 #pragma unroll
                 for (int k = 0; k < R1; ++k) pre[k] = ld_cg(src + 64 * k);
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(128, MINB) fused7a_kernel(Args A) {
                 for (int k = 0; k < R1; ++k) pre[k] = conjf2(pre[k]);
                 __syncthreads();   // previous tile's readers are done with X2
                 const int jM = j0 + 2 * h + colM;
-                const int sig = (int)((((int64_t)jM * A.beta - ((int64_t)A.Kmod * jM) % D) % D + D) % D);
+                const int sig = (jM * (A.beta - A.Kmod)) & (D - 1);   // (j beta - K j) mod D, D a power of 2
                 float2* Fc = F + (2 * h + colM) * K::FS;
                 // G' in stage-2 order: [j0/8][h][r][m2][col][oi][u]
                 const float2* g = Gq + ((((int64_t)idx * 4 + h) * NR * 16) * 2 + colM) * 64 + iM * 4 + uM;

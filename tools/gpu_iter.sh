@@ -1,6 +1,5 @@
 set -x
-CFG=5 ENVS="NSDGT_FUSED=7;NSDGT_FUSED=7" timeout 300 python tools/v7env.py > gpurun_out/env5.log 2>&1
-for v in NOFR NOG ALL; do
-CFG=5 ENVS="NSDGT_FUSED=7;NSDGT_DBG=4" timeout 300 bash tools/altlib_run.sh tools/libnsdgt_xp_$v.so > gpurun_out/env5_$v.log 2>&1
-done
+timeout 600 python -m pytest tests/test_gpu_inverse.py tests/test_gpu_fused7.py -x -q > gpurun_out/t_it.log 2>&1; echo rc=$? >> gpurun_out/t_it.log
+timeout 300 python bench.py --inverse --steps 10 --no-e2e --no-cpu-baseline > gpurun_out/inv5.json 2>/dev/null
+timeout 300 python bench.py --config 3 --inverse --steps 20 --no-e2e --no-cpu-baseline > gpurun_out/inv3.json 2>/dev/null
 echo done
