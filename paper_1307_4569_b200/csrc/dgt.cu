@@ -438,6 +438,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
     }
 }
 
+#include "zak_rr.cuh"
+
 struct OutArgs {
     const void* C;  // [W][iM][q][d]
     void* out;      // [W][M][N]
@@ -1296,6 +1298,7 @@ struct Plan {
     int zct = 0;             // zak_kernel compile-time inner length (0 = runtime radices)
     int inv_generic = 0;     // experiment knob (NSDGT_INV_GENERIC, read at plan time): generic synthesis
     int outct = 0;           // out_kernel compile-time inner channel count (0 = runtime radices)
+    int zrr = 0;             // forward Zak with zak_rr_kernel (d = 180 = 12 x 15 in registers)
     int zsmall = 0;          // forward zak_ct with 128-thread CTAs of RB / 2 columns (c128, d = 180)
     int cnj = 0;             // zak_ct -> out_f4096 intermediate in [n][j] layout
     int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
@@ -1572,7 +1575,9 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
-    if (P->zsmall && sizeof(C) == 16)
+    if (P->zrr)
+        zak_rr_kernel<T, 8, kZrrMinB><<<dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc), 128, zrr_smem<T>(), st>>>(A);
+    else if (P->zsmall && sizeof(C) == 16)
         zak_ct_kernel<T, 180, 4, 2, 128><<<dim3(2 * nrb * (unsigned)I.q, (unsigned)Wc), 128, P->smemA / 2, st>>>(A);
     else if (P->zct == 180 && sizeof(C) == 16)
         zak_ct_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
@@ -1655,6 +1660,9 @@ static int configure(Plan* P, int64_t max_chunk) {
         // barriers than 2 CTAs of 8 warps (config 4: 0.497 -> 0.474 ms per 16 signals); the
         // adjoint measured slower that way (0.492 -> 0.527) and keeps RB
         P->zsmall = (P->zct == 180 && e == 16 && !std::getenv("NSDGT_ZCT_BIG")) ? 1 : 0;
+        // register-resident DFT_180 passes (zak_rr.cuh), 8 residues per 128-thread CTA;
+        // NSDGT_ZAK_CT keeps zak_ct (A/B experiment)
+        P->zrr = (P->zct == 180 && I.c % 8 == 0 && !std::getenv("NSDGT_ZAK_CT")) ? 1 : 0;
     }
     if (P->zct) {
         // the constant-memory twiddles of fft_ct (same values for every plan; long-double
@@ -1689,6 +1697,7 @@ static int configure(Plan* P, int64_t max_chunk) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 720, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA / 2));
+        CUDA_TRY(cudaFuncSetAttribute(zak_rr_kernel<T, 8, kZrrMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zrr_smem<T>()));
     }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     // compile-time output DFT for M' = 200 (config 2, time shear)
