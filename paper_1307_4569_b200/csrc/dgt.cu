@@ -144,6 +144,16 @@ __global__ void k_twiddles(cx<T>* tw, int64_t n) {
     }
 }
 
+// W_n^k for k < count (a prefix of the length-n table)
+template <typename T>
+__global__ void k_twiddles_prefix(cx<T>* tw, int64_t n, int64_t count) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+        double s, c;
+        sincospi(-2.0 * (double)k / (double)n, &s, &c);
+        tw[k] = mk<T>((T)c, (T)s);
+    }
+}
+
 // T-branch post tables (Alg. 1 lines 8-12): E(n) = exp(i pi (C1 n^2 mod 2N)/N) and the
 // row rotation rot(n) = ceil(s1 a n / b) mod M (the printed ((-s1 n a + m b) mod L) div b
 // equals (m - rot(n)) mod M; reading Z5).
@@ -1299,6 +1309,8 @@ struct Plan {
     int inv_generic = 0;     // experiment knob (NSDGT_INV_GENERIC, read at plan time): generic synthesis
     int outct = 0;           // out_kernel compile-time inner channel count (0 = runtime radices)
     int zrr = 0;             // forward Zak with zak_rr_kernel (d = 180 = 12 x 15 in registers)
+    int front = 0;           // F-branch front end by front_f4096_kernel + zak_rr0_kernel (L = 180 x 4096)
+    void* twL = nullptr;     // W_L^e, e < 180 * 256 (front_f4096_kernel)
     int zsmall = 0;          // forward zak_ct with 128-thread CTAs of RB / 2 columns (c128, d = 180)
     int cnj = 0;             // zak_ct -> out_f4096 intermediate in [n][j] layout
     int outk = 0;            // output kernel: 0 generic, 1 out_f4096 (F-branch, iM = 4096)
@@ -1323,10 +1335,10 @@ struct Plan {
 };
 
 enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_ZAKADJ = 6,
-                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_COUNT = 10 };
+                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_FRONTF = 10, PK_COUNT = 11 };
 static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
                                            "zak_ct", "out_f4096", "zak_adjoint", "out_adjoint",
-                                           "fused7a_t_p1", "multiwindow_interleave"};
+                                           "fused7a_t_p1", "multiwindow_interleave", "front_f4096"};
 
 static cudaEvent_t prof_event(Plan* P) {
     if (P->pool_used == P->pool.size()) {
@@ -1367,7 +1379,7 @@ static void free_plan(Plan* P) {
     if (P->inv_alias & 2) P->finv = nullptr;
     void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
                     P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv, P->gt64,
-                    P->scrA, P->scrB};
+                    P->scrA, P->scrB, P->twL};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     free_fast(&P->fp);
@@ -1473,6 +1485,10 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
     k_twiddles<T><<<grid_for(I.d), 256, 0, st>>>((C*)P->tw_d, I.d);
     CUDA_TRY(cudaMalloc(&P->tw_m, sizeof(C) * I.iM));
     k_twiddles<T><<<grid_for(I.iM), 256, 0, st>>>((C*)P->tw_m, I.iM);
+    if (P->front) {
+        CUDA_TRY(cudaMalloc(&P->twL, sizeof(C) * 180 * 256));
+        k_twiddles_prefix<T><<<grid_for(180 * 256), 256, 0, st>>>((C*)P->twL, I.L, 180 * 256);
+    }
     if (I.branch != DGT_BRANCH_FREQ) {
         CUDA_TRY(cudaMalloc(&P->E, sizeof(C) * I.N));
         CUDA_TRY(cudaMalloc(&P->rot, sizeof(int) * I.N));
@@ -1527,6 +1543,16 @@ static int launch_front(Plan* P, const void* f, int64_t nb, cudaStream_t st) {
     const bool real_in = (P->flags & DGT_REAL_INPUT) != 0;
     const double e = (double)sizeof(C), ein = real_in ? e / 2 : e, L = (double)I.L;
     const int ph = prof_open(P, st);
+    if (P->front) {
+        FrontArgs FA{};
+        FA.f = f; FA.real_in = real_in ? 1 : 0; FA.pre = P->pre; FA.H = P->fhat;
+        FA.tw = P->tw_m; FA.twL = P->twL; FA.L = I.L;
+        front_f4096_kernel<T, 2><<<dim3(180, (unsigned)nb), 256, kFrontElems * sizeof(C), st>>>(FA);
+        // a length-4096 DFT of 180 residues per signal (the DFT_180 runs in zak_rr0_kernel)
+        prof_close(P, ph, PK_FRONTF, nb * L * ein + nb * L * e, nb * 5.0 * L * 12.0, st);
+        CUDA_TRY(cudaGetLastError());
+        return DGT_OK;
+    }
     const void* fin = f;
     if (real_in || P->pre) {
         k_prechirp<T><<<grid_for(nb * I.L), 256, 0, st>>>((C*)P->fhat, f, real_in ? 1 : 0, (const C*)P->pre, I.L,
@@ -1575,7 +1601,9 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
-    if (P->zrr)
+    if (P->front)
+        zak_rr0_kernel<T, 8, kZrr0MinB><<<dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc), 128, zrr_smem<T>(), st>>>(A);
+    else if (P->zrr)
         zak_rr_kernel<T, 8, kZrrMinB><<<dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc), 128, zrr_smem<T>(), st>>>(A);
     else if (P->zsmall && sizeof(C) == 16)
         zak_ct_kernel<T, 180, 4, 2, 128><<<dim3(2 * nrb * (unsigned)I.q, (unsigned)Wc), 128, P->smemA / 2, st>>>(A);
@@ -1663,6 +1691,11 @@ static int configure(Plan* P, int64_t max_chunk) {
         // register-resident DFT_180 passes (zak_rr.cuh), 8 residues per 128-thread CTA;
         // NSDGT_ZAK_CT keeps zak_ct (A/B experiment)
         P->zrr = (P->zct == 180 && I.c % 8 == 0 && !std::getenv("NSDGT_ZAK_CT")) ? 1 : 0;
+        // frequency shear with L = 180 x 4096 = d x (c q): the length-L FFT as front_f4096_kernel
+        // (4096-point DFTs of the 180 residues) + one DFT_180 pass pair inside the Zak kernel
+        // (NSDGT_FRONT_CUFFT keeps cuFFT, A/B experiment)
+        P->front = (P->zrr && I.branch == DGT_BRANCH_FREQ && I.L == 180 * 4096 && I.c * I.q == 4096 &&
+                    !std::getenv("NSDGT_FRONT_CUFFT")) ? 1 : 0;
     }
     if (P->zct) {
         // the constant-memory twiddles of fft_ct (same values for every plan; long-double
@@ -1698,6 +1731,9 @@ static int configure(Plan* P, int64_t max_chunk) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 720, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA / 2));
         CUDA_TRY(cudaFuncSetAttribute(zak_rr_kernel<T, 8, kZrrMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zrr_smem<T>()));
+        CUDA_TRY(cudaFuncSetAttribute(zak_rr0_kernel<T, 8, kZrr0MinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zrr_smem<T>()));
+        CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(kFrontElems * e)));
     }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     // compile-time output DFT for M' = 200 (config 2, time shear)

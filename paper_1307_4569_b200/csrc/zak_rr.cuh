@@ -25,6 +25,10 @@
 #define NSDGT_ZRR_MINB 4
 #endif
 constexpr int kZrrMinB = NSDGT_ZRR_MINB;   // CTAs per SM the register budget is sized for
+#ifndef NSDGT_ZRR0_MINB
+#define NSDGT_ZRR0_MINB 3
+#endif
+constexpr int kZrr0MinB = NSDGT_ZRR0_MINB;
 // dynamic shared memory of zak_rr_kernel<T, 8, *>: the twiddle table and two exchange buffers
 template <typename T> constexpr int zrr_smem() { return (180 + 2 * 8 * 180) * (int)sizeof(cx<T>); }
 
@@ -117,3 +121,197 @@ __global__ void __launch_bounds__(16 * RBC, MINB) zak_rr_kernel(ZakArgs A) {
     }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Frequency-shear front end for L = 180 x 4096 (config 4) without cuFFT: the length-L FFT of
+// Alg. 1 line 23 (f^ = fft(pchirp(L, s1) f)) split as l = 180 q + r, nu = x + 4096 j:
+//   f^(x + 4096 j) = sum_r W_180^{r j} H(r, x),   H(r, x) = W_L^{r x} sum_q f(180 q + r) W_4096^{q x}
+// front_f4096_kernel computes H (one CTA per residue r and signal: a 4096-point DFT in three
+// register radix-16 passes, the W_L^{r x} twiddle, contiguous stores H[w][r][x]);
+// zak_rr0_kernel runs the DFT_180 over r as one more register pass pair in front of the Zak
+// kernel's two DFTs, so f^ never exists in memory.
+// ---------------------------------------------------------------------------------------
+struct FrontArgs {
+    const void* f;      // [W][L] input (complex, or real with real_in)
+    int real_in;
+    const void* pre;    // [L] pchirp(L, s1) multiplier (nullable)
+    void* H;            // [W][180][4096] output
+    const void* tw;     // W_4096^k, k < 4096
+    const void* twL;    // W_L^e, e < 180 * 256
+    int64_t L;
+};
+constexpr int kFrontElems = 256 * 17;   // exchange buffer (elements), padded for pass 3
+
+// v[k] *= b0 * w^k, k < 16 (w^k from three squarings and products: <= 6 roundings)
+template <typename C>
+__device__ __forceinline__ void twiddle16b(C* v, C b0, C w1) {
+    const C w2 = cmul(w1, w1), w4 = cmul(w2, w2), w8 = cmul(w4, w4);
+    C p[16];
+    p[0] = b0; p[1] = cmul(b0, w1); p[2] = cmul(b0, w2); p[4] = cmul(b0, w4); p[8] = cmul(b0, w8);
+    p[3] = cmul(p[1], w2); p[5] = cmul(p[1], w4); p[6] = cmul(p[2], w4); p[7] = cmul(p[3], w4);
+#pragma unroll
+    for (int k = 9; k < 16; ++k) p[k] = cmul(p[k - 8], w8);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = cmul(v[k], p[k]);
+}
+
+// 4096-point DFT, q = q0 + 16 q1 + 256 q2 -> x = x0 + 16 x1 + 256 x2:
+//   pass 1, lane (q0, q1): A = W_256^{q1 x0} sum_q2 W_16^{q2 x0} g(q)
+//   pass 2, lane (q0, x0): B = W_4096^{q0 (x0 + 16 x1)} sum_q1 W_16^{q1 x1} A
+//   pass 3, lane (x0, x1): X(x0 + 16 x1 + 256 x2) = sum_q0 W_16^{q0 x2} B     (lane = x mod 256)
+template <typename T, int MINB>
+__global__ void __launch_bounds__(256, MINB) front_f4096_kernel(FrontArgs A) {
+    using C = cx<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* S = (C*)smem_raw;
+    const int tid = threadIdx.x;
+    const int r = blockIdx.x;
+    const int64_t w = blockIdx.y;
+    const C* __restrict__ tw = (const C*)A.tw;
+    C v[16];
+    {
+        const int64_t base = w * A.L + r;
+        const C* __restrict__ pre = (const C*)A.pre;
+#pragma unroll
+        for (int q2 = 0; q2 < 16; ++q2) {
+            const int l = 180 * (tid + 256 * q2);
+            v[q2] = A.real_in ? mk<T>(((const T*)A.f)[base + l], T(0)) : ((const C*)A.f)[base + l];
+        }
+        if (pre) {
+#pragma unroll
+            for (int q2 = 0; q2 < 16; ++q2) v[q2] = cmul(v[q2], __ldg(pre + r + 180 * (tid + 256 * q2)));
+        }
+    }
+    dft16<T>(v);
+    {
+        const int q1 = tid >> 4;
+        if (q1) twiddle16b(v, mk<T>(T(1), T(0)), __ldg(tw + 16 * q1));
+    }
+#pragma unroll
+    for (int x0 = 0; x0 < 16; ++x0) S[x0 * 256 + tid] = v[x0];
+    __syncthreads();
+    {
+        const int q0 = tid & 15, x0 = tid >> 4;
+#pragma unroll
+        for (int q1 = 0; q1 < 16; ++q1) v[q1] = S[x0 * 256 + q0 + 16 * q1];
+        __syncthreads();
+        dft16<T>(v);
+        if (q0) twiddle16b(v, __ldg(tw + q0 * x0), __ldg(tw + 16 * q0));
+        // B(q0, x1, x0) at (x1 * 16 + x0) * 17 + q0
+#pragma unroll
+        for (int x1 = 0; x1 < 16; ++x1) S[(x1 * 16 + x0) * 17 + q0] = v[x1];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q0 = 0; q0 < 16; ++q0) v[q0] = S[tid * 17 + q0];
+    dft16<T>(v);
+    // H(r, x) = W_L^{r x} X(x), x = tid + 256 x2: W_L^{r tid} (W_L^{256 r})^{x2}
+    twiddle16b(v, __ldg((const C*)A.twL + r * tid), __ldg((const C*)A.twL + 256 * r));
+    C* H = (C*)A.H + w * A.L + (int64_t)r * 4096;
+#pragma unroll
+    for (int x2 = 0; x2 < 16; ++x2) H[tid + 256 * x2] = v[x2];
+}
+
+// zak_rr_kernel with the front end's DFT_180 over r in front (config 4 without cuFFT):
+//   stage 0, r = 12 a + b -> j = p + 15 k:  f^(x + 4096 j), x = r0 + rr + c l
+//     b-thread: DFT_15 over a, W180^{b p}; exchange; p-thread: DFT_12 over b; chirp on j
+//   stage 1 (Zak DFT), j = p + 15 k -> nu = t + 12 e:
+//     p-thread: DFT_12 over k, W180^{p t}; exchange; t-thread: DFT_15 over p -> Phi(t + 12 e)
+//   stage 2 per u (factor DFT), nu = t + 12 e -> tau = p + 15 k:
+//     t-thread: products, DFT_15 over e, W180^{t p}; exchange; p-thread: DFT_12 over t, scatter
+// 6 barriers per CTA; Phi (15 values) stays in the t-threads' registers.
+template <typename T, int RBC, int MINB>
+__global__ void __launch_bounds__(16 * RBC, MINB) zak_rr0_kernel(ZakArgs A) {
+    constexpr int D = 180, Q = 4;
+    using C = cx<T>;
+    static_assert((12 * RBC) % 32 == 0, "the 12-lane groups are whole warps (named barrier 1)");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* tws = (C*)smem_raw;
+    C* X0 = tws + D;
+    C* X1 = X0 + RBC * D;
+    const int c = (int)A.c;
+    const int nrb = c / RBC;
+    const int rblk = blockIdx.x % nrb, l = blockIdx.x / nrb;
+    const int64_t w = blockIdx.y;
+    const int r0 = rblk * RBC;
+    const int tid = threadIdx.x;
+    const int rr = tid % RBC, hi = tid / RBC;
+    const int x = r0 + rr + c * l;            // column of H / f^ (x < 4096)
+    // ---- stage 0, pass 1 (b-threads): H(12 a + b, x), DFT_15 over a ----
+    if (hi < 12) {
+        const int b = hi;
+        const C* Hc = (const C*)A.f + w * A.L + (int64_t)b * 4096 + x;
+        C v[15];
+#pragma unroll
+        for (int a = 0; a < 15; ++a) v[a] = Hc[a * 12 * 4096];
+        for (int i = tid; i < D; i += 12 * RBC) tws[i] = ((const C*)A.tw)[i];
+        dft_pq<T, 3, 5, 180>(v, 12);
+        asm volatile("bar.sync 1, %0;" ::"r"(12 * RBC) : "memory");
+#pragma unroll
+        for (int p = 0; p < 15; ++p) X0[(b * 15 + p) * RBC + rr] = p ? cmul(v[p], tws[b * p]) : v[p];
+    }
+    __syncthreads();
+    // ---- stage 0, pass 2 + stage 1, pass 1 (p-threads) ----
+    if (hi < 15) {
+        const int p = hi;
+        C e[12];
+#pragma unroll
+        for (int b = 0; b < 12; ++b) e[b] = X0[(b * 15 + p) * RBC + rr];
+        dft_pq<T, 4, 3, 180>(e, 15);     // e[k] = f^(x + 4096 (p + 15 k))
+        const C* __restrict__ chirp = (const C*)A.chirp;
+        if (chirp) {
+#pragma unroll
+            for (int k = 0; k < 12; ++k) e[k] = cmul(e[k], __ldg(chirp + x + 4096 * (p + 15 * k)));
+        }
+        dft_pq<T, 4, 3, 180>(e, 15);     // over k -> t
+#pragma unroll
+        for (int t = 0; t < 12; ++t) X1[(p * 12 + t) * RBC + rr] = t ? cmul(e[t], tws[p * t]) : e[t];
+    }
+    __syncthreads();
+    // ---- stage 1, pass 2 (t-threads): Phi(t + 12 e), e < 15 ----
+    C ph[15];
+    if (hi < 12) {
+        const int t = hi;
+#pragma unroll
+        for (int p = 0; p < 15; ++p) ph[p] = X1[(p * 12 + t) * RBC + rr];
+        dft_pq<T, 3, 5, 180>(ph, 12);
+    }
+    const C* __restrict__ G = (const C*)A.G + (int64_t)(r0 + rr) * Q * D;
+    C* Cw = (C*)A.C + w * A.iM * Q * D;
+    const int jbase = r0 + c * (l % Q);
+    const int iM = (int)A.iM;
+#pragma unroll 1
+    for (int u = 0; u < Q; ++u) {
+        C* Xu = (u & 1) ? X1 : X0;
+        if (hi < 12) {
+            const int t = hi;
+            C y[15];
+#pragma unroll
+            for (int e = 0; e < 15; ++e) y[e] = __ldg(G + u * D + t + 12 * e);
+#pragma unroll
+            for (int e = 0; e < 15; ++e) y[e] = cmul(ph[e], y[e]);
+            dft_pq<T, 3, 5, 180>(y, 12);  // over e -> p
+#pragma unroll
+            for (int p = 0; p < 15; ++p) Xu[(t * 15 + p) * RBC + rr] = p ? cmul(y[p], tws[t * p]) : y[p];
+        }
+        __syncthreads();
+        if (hi < 15) {
+            const int p = hi;
+            C z[12];
+#pragma unroll
+            for (int t = 0; t < 12; ++t) z[t] = Xu[(t * 15 + p) * RBC + rr];
+            dft_pq<T, 4, 3, 180>(z, 15);  // over t -> k: Y(p + 15 k)
+            const int kappa = (l - u + Q) % Q;
+            const int off = l < u ? 1 : 0;
+#pragma unroll
+            for (int k = 0; k < 12; ++k) {
+                const int tau = p + 15 * k;
+                int np = D - tau - off;
+                if (np >= D) np -= D;
+                if (np < 0) np += D;
+                if (A.cnj) Cw[(int64_t)(kappa + Q * np) * iM + jbase + rr] = z[k];
+                else Cw[((jbase + rr) * Q + kappa) * D + np] = z[k];
+            }
+        }
+    }
+}
