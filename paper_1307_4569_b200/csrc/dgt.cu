@@ -1335,10 +1335,10 @@ struct Plan {
 };
 
 enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_ZAKADJ = 6,
-                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_FRONTF = 10, PK_COUNT = 11 };
+                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_FRONTF = 10, PK_ZAKRR = 11, PK_COUNT = 12 };
 static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
                                            "zak_ct", "out_f4096", "zak_adjoint", "out_adjoint",
-                                           "fused7a_t_p1", "multiwindow_interleave", "front_f4096"};
+                                           "fused7a_t_p1", "multiwindow_interleave", "front_f4096", "zak_rr"};
 
 static cudaEvent_t prof_event(Plan* P) {
     if (P->pool_used == P->pool.size()) {
@@ -1547,9 +1547,10 @@ static int launch_front(Plan* P, const void* f, int64_t nb, cudaStream_t st) {
         FrontArgs FA{};
         FA.f = f; FA.real_in = real_in ? 1 : 0; FA.pre = P->pre; FA.H = P->fhat;
         FA.tw = P->tw_m; FA.twL = P->twL; FA.L = I.L;
-        front_f4096_kernel<T, 2><<<dim3(180, (unsigned)nb), 256, kFrontElems * sizeof(C), st>>>(FA);
+        front_f4096_kernel<T, 2 / kFrontRes, kFrontRes>
+            <<<dim3(180 / kFrontRes, (unsigned)nb), 256 * kFrontRes, front_smem(sizeof(C)), st>>>(FA);
         // a length-4096 DFT of 180 residues per signal (the DFT_180 runs in zak_rr0_kernel)
-        prof_close(P, ph, PK_FRONTF, nb * L * ein + nb * L * e, nb * 5.0 * L * 12.0, st);
+        prof_close(P, ph, PK_FRONTF, nb * L * ein, nb * 5.0 * L * 12.0, st);
         CUDA_TRY(cudaGetLastError());
         return DGT_OK;
     }
@@ -1615,7 +1616,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
         zak_ct_kernel<T, 720, 4, 1><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
     else
         zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->gA ? 0 : P->smemA, st>>>(A);
-    prof_close(P, ph, P->zct ? PK_ZAKCT : PK_ZAK, by_in, fl_zak, st);
+    prof_close(P, ph, (P->zrr || P->front) ? PK_ZAKRR : P->zct ? PK_ZAKCT : PK_ZAK, by_in, fl_zak, st);
     const OutArgs B = make_out_args(P, P->Cws, c);
     const int ntiles = B.grouped ? (int)(I.q * ((I.d + P->NT - 1) / P->NT)) : (int)((I.iN + P->NT - 1) / P->NT);
     ph = prof_open(P, st);
@@ -1732,8 +1733,8 @@ static int configure(Plan* P, int64_t max_chunk) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA / 2));
         CUDA_TRY(cudaFuncSetAttribute(zak_rr_kernel<T, 8, kZrrMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zrr_smem<T>()));
         CUDA_TRY(cudaFuncSetAttribute(zak_rr0_kernel<T, 8, kZrr0MinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zrr_smem<T>()));
-        CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(kFrontElems * e)));
+        CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem((int)e)));
     }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     // compile-time output DFT for M' = 200 (config 2, time shear)
@@ -2571,9 +2572,9 @@ int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W) {
     const int64_t chunks = (W + P->chunk - 1) / P->chunk;
     const int64_t per = P->fast ? fast_launches_per_chunk(&P->fp) + 1 /* counter memset */ : 2;
     int64_t n = chunks * per;
-    // F-branch: per front batch the pre-chirp kernel when needed (the cuFFT call's own
-    // kernels are library launches and not counted)
-    if (P->info.branch == DGT_BRANCH_FREQ && !P->fast && (((P->flags & DGT_REAL_INPUT) || P->pre)))
+    // F-branch: per front batch front_f4096, or the pre-chirp kernel when needed (the cuFFT
+    // call's own kernels are library launches and not counted)
+    if (P->info.branch == DGT_BRANCH_FREQ && !P->fast && (P->front || (P->flags & DGT_REAL_INPUT) || P->pre))
         n += (W + P->fb - 1) / P->fb;
     return n;
 }

@@ -140,7 +140,12 @@ struct FrontArgs {
     const void* twL;    // W_L^e, e < 180 * 256
     int64_t L;
 };
-constexpr int kFrontElems = 256 * 17;   // exchange buffer (elements), padded for pass 3
+constexpr int kFrontElems = 256 * 17;   // exchange buffer per residue (elements), padded for pass 3
+#ifndef NSDGT_FRONT_RES
+#define NSDGT_FRONT_RES 2
+#endif
+constexpr int kFrontRes = NSDGT_FRONT_RES;   // residues per front_f4096 CTA
+constexpr int front_smem(int esz) { return (kFrontRes * (kFrontElems + 4)) * esz; }
 
 // v[k] *= b0 * w^k, k < 16 (w^k from three squarings and products: <= 6 roundings)
 template <typename C>
@@ -155,17 +160,35 @@ __device__ __forceinline__ void twiddle16b(C* v, C b0, C w1) {
     for (int k = 0; k < 16; ++k) v[k] = cmul(v[k], p[k]);
 }
 
+// v[k] *= w^k, k < 16
+template <typename C>
+__device__ __forceinline__ void twiddle16(C* v, C w1) {
+    const C w2 = cmul(w1, w1), w4 = cmul(w2, w2), w8 = cmul(w4, w4);
+    C p[16];
+    p[1] = w1; p[2] = w2; p[4] = w4; p[8] = w8;
+    p[3] = cmul(w1, w2); p[5] = cmul(w1, w4); p[6] = cmul(w2, w4); p[7] = cmul(p[3], w4);
+#pragma unroll
+    for (int k = 9; k < 16; ++k) p[k] = cmul(p[k - 8], w8);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) v[k] = cmul(v[k], p[k]);
+}
+
 // 4096-point DFT, q = q0 + 16 q1 + 256 q2 -> x = x0 + 16 x1 + 256 x2:
 //   pass 1, lane (q0, q1): A = W_256^{q1 x0} sum_q2 W_16^{q2 x0} g(q)
 //   pass 2, lane (q0, x0): B = W_4096^{q0 (x0 + 16 x1)} sum_q1 W_16^{q1 x1} A
 //   pass 3, lane (x0, x1): X(x0 + 16 x1 + 256 x2) = sum_q0 W_16^{q0 x2} B     (lane = x mod 256)
-template <typename T, int MINB>
-__global__ void __launch_bounds__(256, MINB) front_f4096_kernel(FrontArgs A) {
+// RES residues per CTA of 256 RES threads, lane = (t, h) with h = tid mod RES fastest: the
+// RES samples f(180 q + r0 + h) of a lane pair are adjacent (RES = 2: 32-byte sectors used
+// whole instead of half), each residue has its own exchange buffer (offset by 4 elements so the
+// two halves of a quarter warp hit different banks).
+template <typename T, int MINB, int RES>
+__global__ void __launch_bounds__(256 * RES, MINB) front_f4096_kernel(FrontArgs A) {
     using C = cx<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    C* S = (C*)smem_raw;
-    const int tid = threadIdx.x;
-    const int r = blockIdx.x;
+    const int tid = threadIdx.x % (256 * RES) / RES;   // t
+    const int h = threadIdx.x % RES;
+    C* S = (C*)smem_raw + h * (kFrontElems + 4);
+    const int r = blockIdx.x * RES + h;
     const int64_t w = blockIdx.y;
     const C* __restrict__ tw = (const C*)A.tw;
     C v[16];
@@ -185,7 +208,7 @@ __global__ void __launch_bounds__(256, MINB) front_f4096_kernel(FrontArgs A) {
     dft16<T>(v);
     {
         const int q1 = tid >> 4;
-        if (q1) twiddle16b(v, mk<T>(T(1), T(0)), __ldg(tw + 16 * q1));
+        if (q1) twiddle16(v, __ldg(tw + 16 * q1));
     }
 #pragma unroll
     for (int x0 = 0; x0 < 16; ++x0) S[x0 * 256 + tid] = v[x0];

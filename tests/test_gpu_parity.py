@@ -207,6 +207,59 @@ def test_config4_lattice_c64_sampled(torch_cuda, nsdgt, oracle_mod):
 
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_config4_front_and_zak_variants_agree(torch_cuda, nsdgt, oracle_mod, dtype, monkeypatch):
+    """Config 4 runs front_f4096 + zak_rr0 (the length-L FFT split as 4096-point DFTs of the
+    180 residues and a DFT_180 inside the Zak kernel; no cuFFT).  The same plan with cuFFT's
+    front end + zak_rr (NSDGT_FRONT_CUFFT) and with cuFFT + the Stockham zak_ct (also
+    NSDGT_ZAK_CT) agree with it and with the oracle on sampled columns."""
+    torch = torch_cuda
+    wl = CONFIGS[3]
+    g = window(wl)
+    fnp = batch(wl, 0, 2).astype(np.complex64 if dtype == "c64" else np.complex128)
+    f = torch.from_numpy(fnp).cuda()
+    p = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
+    p.profile_begin()
+    c = p.execute(f)
+    names = {k["name"] for k in p.profile_end()}
+    assert "front_f4096" in names and "front_fft_cufft" not in names, names
+    monkeypatch.setenv("NSDGT_FRONT_CUFFT", "1")
+    c1 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype).execute(f)
+    monkeypatch.setenv("NSDGT_ZAK_CT", "1")
+    c2 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype).execute(f)
+    tol = TOL[dtype]
+    assert rel(c.cpu().numpy(), c1.cpu().numpy()) <= tol
+    assert rel(c.cpu().numpy(), c2.cpu().numpy()) <= tol
+    cols = np.sort(np.random.default_rng(45).choice(wl.N, 16, replace=False))
+    ref = oracle_mod.dgt(fnp, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols)
+    assert rel(c[:, :, torch.from_numpy(cols).cuda()].cpu().numpy(), ref) <= tol
+
+
+@pytest.mark.parametrize("lam", [(1, 3), (1, 6)])
+def test_front_f4096_real_input_and_prechirp(torch_cuda, nsdgt, oracle_mod, lam):
+    """front_f4096's real-input load and its pchirp(L, s1) multiplier: config 4's lattice with
+    real f (lambda = 1/3, s1 = 0) and lambda = 1/6 (s1 = 128, the pre-chirp), both on the
+    front_f4096 path, sampled columns against the oracle."""
+    torch = torch_cuda
+    wl = CONFIGS[3]
+    l1, l2 = lam
+    info = nsdgt.lattice_plan(wl.L, wl.a, wl.M, l1, l2)
+    assert info["d"] == 180 and info["c"] * info["q"] == 4096
+    g = window(wl)
+    fc = batch(wl, 0, 1)
+    f = np.ascontiguousarray(fc.real) if lam == (1, 3) else fc
+    if lam == (1, 6):
+        assert info["pre_sigma"] != 0
+    p = nsdgt.Plan(wl.L, wl.a, wl.M, l1, l2, g, dtype="c128", real_input=np.isrealobj(f))
+    p.profile_begin()
+    c = p.execute(torch.from_numpy(f).cuda())
+    assert "front_f4096" in {k["name"] for k in p.profile_end()}
+    N = wl.L // wl.a
+    cols = np.sort(np.random.default_rng(46).choice(N, 12, replace=False))
+    ref = oracle_mod.dgt(f, g, wl.a, wl.M, l1, l2, cols=cols)
+    assert rel(c[:, :, torch.from_numpy(cols).cuda()].cpu().numpy(), ref) <= TOL["c128"]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_config4_intermediate_layouts_bitwise_equal(torch_cuda, nsdgt, dtype, monkeypatch):
     """zak_ct -> out_f4096 on config 4 store the intermediate [n][j] (contiguous output-kernel
     loads); the generic [j][kappa][n'] layout (NSDGT_CNJ_OFF) runs the same arithmetic, so

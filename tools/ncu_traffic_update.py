@@ -12,6 +12,7 @@ import sys
 # CUDA kernel name prefix -> the profile kind of dgt.cu's prof_close (bench.py's kernel names)
 KINDS = [("fused7a_kernel", "fused7a_t_p1"), ("fused7_kernel", "fused7_t_p1"),
          ("zak_ct_adj_kernel", "zak_adjoint"), ("zak_ct_kernel", "zak_ct"),
+         ("zak_rr0_kernel", "zak_rr"), ("zak_rr_kernel", "zak_rr"), ("front_f4096_kernel", "front_f4096"),
          ("out_f4096_adj_kernel", "out_adjoint"), ("out_f4096_kernel", "out_f4096"),
          ("zak_adj_kernel", "zak_adjoint"), ("out_adj_kernel", "out_adjoint"),
          ("zak_kernel", "zak_generic"), ("out_kernel", "out_generic")]
