@@ -725,6 +725,8 @@ __global__ void __launch_bounds__(256, MINB) out_f4096_kernel(OutArgs A) {
 }
 constexpr size_t kOutF4096Elems = 16 * 272;
 
+#include "tiny.cuh"
+
 // ---------------------------------------------------------------------------------
 // synthesis (the inverse DGT with the plan's window as the synthesis window gamma; SURVEY
 // NEXT-1): f = sum_{m,n} c(m,n) M_{b(m+w(n))} T_{an} gamma, the inversion formula of
@@ -1310,6 +1312,9 @@ struct Plan {
     int outct = 0;           // out_kernel compile-time inner channel count (0 = runtime radices)
     int zrr = 0;             // forward Zak with zak_rr_kernel (d = 180 = 12 x 15 in registers)
     int front = 0;           // F-branch front end by front_f4096_kernel + zak_rr0_kernel (L = 180 x 4096)
+    int tiny = 0;            // whole transform of a signal in one CTA (tiny.cuh)
+    size_t tiny_smem = 0;
+    Radices rd_L{};
     void* twL = nullptr;     // W_L^e, e < 180 * 256 (front_f4096_kernel)
     int zsmall = 0;          // forward zak_ct with 128-thread CTAs of RB / 2 columns (c128, d = 180)
     int cnj = 0;             // zak_ct -> out_f4096 intermediate in [n][j] layout
@@ -1335,10 +1340,10 @@ struct Plan {
 };
 
 enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_ZAKADJ = 6,
-                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_FRONTF = 10, PK_ZAKRR = 11, PK_COUNT = 12 };
+                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_FRONTF = 10, PK_ZAKRR = 11, PK_TINY = 12, PK_COUNT = 13 };
 static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
                                            "zak_ct", "out_f4096", "zak_adjoint", "out_adjoint",
-                                           "fused7a_t_p1", "multiwindow_interleave", "front_f4096", "zak_rr"};
+                                           "fused7a_t_p1", "multiwindow_interleave", "front_f4096", "zak_rr", "tiny"};
 
 static cudaEvent_t prof_event(Plan* P) {
     if (P->pool_used == P->pool.size()) {
@@ -1485,6 +1490,10 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
     k_twiddles<T><<<grid_for(I.d), 256, 0, st>>>((C*)P->tw_d, I.d);
     CUDA_TRY(cudaMalloc(&P->tw_m, sizeof(C) * I.iM));
     k_twiddles<T><<<grid_for(I.iM), 256, 0, st>>>((C*)P->tw_m, I.iM);
+    if (P->tiny && I.branch == DGT_BRANCH_FREQ) {   // W_L for the one-CTA path's DFT_L
+        CUDA_TRY(cudaMalloc(&P->twL, sizeof(C) * L));
+        k_twiddles<T><<<grid_for(L), 256, 0, st>>>((C*)P->twL, L);
+    }
     if (P->front) {
         CUDA_TRY(cudaMalloc(&P->twL, sizeof(C) * 180 * 256));
         k_twiddles_prefix<T><<<grid_for(180 * 256), 256, 0, st>>>((C*)P->twL, I.L, 180 * 256);
@@ -1751,6 +1760,20 @@ static int configure(Plan* P, int64_t max_chunk) {
                                   (int)(kOutF4096Elems * e)));
     CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kOutF4096Elems * e)));
+    // short signals: the whole transform of a signal in one CTA when its tables and buffers fit
+    // 96 KB of shared memory (config 1); NSDGT_TINY_OFF keeps the chunked kernels
+    {
+        const bool freq = I.branch == DGT_BRANCH_FREQ;
+        const int64_t te = tiny_elems(I.L, I.q, I.p, I.d, I.iM, freq);
+        const Radices rl = make_radices((int)std::min<int64_t>(I.L, 1 << 30));
+        P->tiny = (!std::getenv("NSDGT_TINY_OFF") && te * (int64_t)e <= 96 * 1024 && I.iM * I.iN == I.L / I.p * I.q &&
+                   I.iM == I.c * I.q && rl.nst <= kMaxStages) ? 1 : 0;
+        if (P->tiny) {
+            P->rd_L = rl;
+            P->tiny_smem = (size_t)te * e;
+            CUDA_TRY(cudaFuncSetAttribute(tiny_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->tiny_smem));
+        }
+    }
     P->inv_generic = std::getenv("NSDGT_INV_GENERIC") ? 1 : 0;
     // synthesis kernels (the adjoints of zak_kernel / out_kernel)
     P->smemAinv = (size_t)P->RB * (2 * I.p + 1) * I.d * e;
@@ -2008,10 +2031,41 @@ static int execute_mw(Plan* P, const void* f, void* c, int64_t W, cudaStream_t s
     return DGT_OK;
 }
 
+// One CTA per signal, the whole transform in shared memory (tiny.cuh).
+template <typename T>
+static int launch_tiny(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) {
+    const dgt_lattice_info& I = P->info;
+    TinyArgs TA{};
+    TA.f = f; TA.real_in = (P->flags & DGT_REAL_INPUT) ? 1 : 0; TA.pre = P->pre; TA.chirp = P->chirp; TA.G = P->G;
+    TA.twL = P->twL; TA.twd = P->tw_d; TA.twm = P->tw_m;
+    TA.rdL = P->rd_L; TA.rdd = P->rd_d; TA.rdm = P->rd_m;
+    TA.L = (int)I.L; TA.c = (int)I.c; TA.d = (int)I.d; TA.p = (int)I.p; TA.q = (int)I.q;
+    TA.iM = (int)I.iM; TA.iN = (int)I.iN;
+    TA.B = make_out_args(P, nullptr, c);
+    const double e = (double)P->esz, ein = (P->flags & DGT_REAL_INPUT) ? e / 2 : e;
+    const double L = (double)I.L, MN = (double)I.M * (double)I.N;
+    const double lg_d = std::log2((double)I.d), lg_m = std::log2((double)I.iM);
+    const double fl = W * ((I.branch == DGT_BRANCH_FREQ ? 4.0 * L * std::log2(L) : 0.0) + 8.0 * L * I.q / I.p +
+                           4.0 * L * lg_d + 4.0 * MN * lg_d + 4.0 * MN * lg_m + 6.0 * MN);
+    const int ph = prof_open(P, st);
+    for (int64_t w0 = 0; w0 < W; w0 += 65535 * 1024) {
+        const int64_t wc = std::min<int64_t>(65535 * 1024, W - w0);
+        TinyArgs Tw = TA;
+        Tw.f = (const char*)f + (size_t)w0 * I.L * (size_t)ein;
+        Tw.B.out = (char*)c + (size_t)w0 * I.M * I.N * P->esz;
+        tiny_kernel<T><<<(unsigned)wc, 256, P->tiny_smem, st>>>(Tw);
+    }
+    prof_close(P, ph, PK_TINY, W * (L * ein + MN * e) + L * e, fl, st);
+    CUDA_TRY(cudaGetLastError());
+    return DGT_OK;
+}
+
 static int execute(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
     if (P->ola) return execute_ola(P, f, c, W, st);
     if (!P->mw.empty()) return execute_mw(P, f, c, W, st);
+    if (P->tiny && !P->fast)
+        return P->dtype == DGT_C64 ? launch_tiny<float>(P, f, c, W, st) : launch_tiny<double>(P, f, c, W, st);
     const size_t ein = (P->flags & DGT_REAL_INPUT) ? P->esz / 2 : P->esz;
     if (I.branch == DGT_BRANCH_FREQ && !P->fast) {
         // front batches of P->fb signals (a multiple of the chunk), then the chunks of each
@@ -2569,6 +2623,7 @@ int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W) {
         }
         return n;
     }
+    if (P->tiny && !P->fast) return (W + 65535 * 1024 - 1) / (65535 * 1024);
     const int64_t chunks = (W + P->chunk - 1) / P->chunk;
     const int64_t per = P->fast ? fast_launches_per_chunk(&P->fp) + 1 /* counter memset */ : 2;
     int64_t n = chunks * per;

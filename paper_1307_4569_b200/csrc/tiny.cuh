@@ -1,0 +1,153 @@
+// tiny.cuh -- the whole shear algorithm (Alg. 1, lines 1-31) for one short signal in
+// one CTA: BASELINE config 1 (L = 240) and other lattices whose tables and buffers fit shared
+// memory.  The chunked path runs a pre-chirp kernel, cuFFT and two kernels per chunk, each
+// starting with cold loads of its tables (about 35 us of dependent launches and DRAM round
+// trips for 360 coefficients); here every table is fetched into shared memory in one round at
+// the start and the steps follow in one CTA, each batched over all residues and columns:
+//   0. f (real input promoted), times pchirp(L, s1) in the frequency shear (Alg. 1 line 23)
+//   1. F-branch: f^ = DFT_L (Stockham engine, fft_smem.cuh)
+//   2. Zak gather x = r + c ((k q + p l + s p q) mod L/c) with the chirp on load, all (l, r, k)
+//   3. DFT_d over s of the q c p sequences
+//   4. Y(l, r, u; nu) = sum_k Phi(l, r, k; nu) G(r, u, k; nu) for all (l, r, u)   (Eq. phi)
+//   5. DFT_d over nu of the q c q products, scatter T_r(l, u; tau) to C[n][j]:
+//      j = r + c ((l p) mod q), n = kappa + q n', kappa = (l - u) mod q, n' = (-tau - [l < u]) mod d
+//   6. DFT over j (iM) of the iN columns
+//   7. output: T-branch c[(m - rot n) mod M][n] = E(n) X(m, n); F-branch the Alg. 1 remap
+//      with its phase (the same per-coefficient residues as out_kernel's fb_* helpers)
+// Included inside namespace nsdgt by dgt.cu after the output kernels.
+#pragma once
+
+struct TinyArgs {
+    const void* f;        // [W][L] input (complex, or real with real_in)
+    int real_in;
+    const void* pre;      // F-branch pchirp(L, s1) on f (nullable)
+    const void* chirp;    // chirp on the Zak load (nullable): T-branch P_{s1}, F-branch P_{-s0}
+    const void* G;        // window factors [c][q][p][d]
+    const void* twL;      // W_L^k, k < L (F-branch)
+    const void* twd;      // W_d^k
+    const void* twm;      // W_iM^k
+    Radices rdL, rdd, rdm;
+    int L, c, d, p, q, iM, iN;
+    OutArgs B;            // output constants (out, M, N, E / rot or the F-branch remap)
+};
+
+// shared-memory elements of tiny_kernel (also the host's fit test)
+__host__ __device__ inline int64_t tiny_elems(int64_t L, int64_t q, int64_t p, int64_t d, int64_t iM, bool freq) {
+    const int64_t LQ = L * q / p;   // products / intermediate (= iM iN)
+    const int64_t LX = LQ > L ? LQ : L;   // work buffers: the Zak gather (L) and the products (LQ)
+    return 2 * L + 2 * LX + L /* G */ + L /* chirp */ + (freq ? L : 0) /* twL */ + d + iM;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
+    using C = cx<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int L = A.L, c = A.c, d = A.d, p = A.p, q = A.q, iM = A.iM, iN = A.iN;
+    const bool freq = A.B.branch == DGT_BRANCH_FREQ;
+    const int LQ = L / p * q;
+    const int LX = LQ > L ? LQ : L;
+    C* sF = (C*)smem_raw;        // L
+    C* sF2 = sF + L;             // L
+    C* sX = sF2 + L;             // max(L, LQ)
+    C* sY = sX + LX;             // max(L, LQ)
+    C* sG = sY + LX;             // L
+    C* sCh = sG + L;             // L
+    C* sTwL = sCh + L;           // L (F-branch)
+    C* sTwd = sTwL + (freq ? L : 0);
+    C* sTwm = sTwd + d;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int64_t w = blockIdx.x;
+    // the output-stage tables go to L2 now (read once at the end)
+    if (tid == 0) {
+        const char* e = freq ? (const char*)A.B.ptab : (const char*)A.B.E;
+        if (!e) e = (const char*)A.G;   // (no output table: a harmless re-fetch)
+        const int64_t eb = freq ? 2 * A.B.N * (int64_t)sizeof(C) : A.B.N * (int64_t)sizeof(C);
+        for (int64_t o = 0; o < eb; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(e + o));
+        if (!freq)
+            for (int64_t o = 0; o < A.B.N * 4; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)A.B.rot + o));
+    }
+    // ---- 0. one round of loads: f (x pre), G, chirp, twiddles ----
+    {
+        const C* __restrict__ pre = (const C*)A.pre;
+        const C* __restrict__ chirp = (const C*)A.chirp;
+        for (int i = tid; i < L; i += nt) {
+            C v = A.real_in ? mk<T>(((const T*)A.f)[w * L + i], T(0)) : ((const C*)A.f)[w * L + i];
+            if (pre) v = cmul(v, __ldg(pre + i));
+            sF[i] = v;
+            sG[i] = __ldg((const C*)A.G + i);
+            sCh[i] = chirp ? __ldg(chirp + i) : mk<T>(T(1), T(0));
+            if (freq) sTwL[i] = __ldg((const C*)A.twL + i);
+        }
+        for (int i = tid; i < d; i += nt) sTwd[i] = __ldg((const C*)A.twd + i);
+        for (int i = tid; i < iM; i += nt) sTwm[i] = __ldg((const C*)A.twm + i);
+    }
+    __syncthreads();
+    // ---- 1. F-branch: f^ = DFT_L(f) ----
+    const C* fh = freq ? fft_smem<T>(sF, sF2, A.rdL, 1, L, sTwL) : sF;
+    // ---- 2. Zak gather of all (l, r, k, s): sX[((l c + r) p + k) d + s] ----
+    {
+        const int Lc = L / c;
+        for (int i = tid; i < L; i += nt) {
+            const int s = i % d, t = i / d;          // t = (l c + r) p + k
+            const int k = t % p, lr = t / p;
+            const int r = lr % c, l = lr / c;
+            const int z = (k * q + p * l + s * p * q) % Lc;
+            const int x = r + c * z;
+            sX[i] = cmul(fh[x], sCh[x]);
+        }
+    }
+    __syncthreads();
+    // ---- 3. DFT_d over s ----
+    C* phi = fft_smem<T>(sX, sY, A.rdd, q * c * p, d, sTwd);
+    C* Yb = phi == sX ? sY : sX;
+    // ---- 4. products Y(l, r, u; nu) at Yb[((l c + r) q + u) d + nu] ----
+    for (int i = tid; i < LQ; i += nt) {
+        const int nu = i % d, t = i / d;              // t = (l c + r) q + u
+        const int u = t % q, lr = t / q;
+        const int r = lr % c;
+        const C* ph = phi + lr * p * d + nu;
+        const C* gk = sG + (r * q + u) * p * d + nu;
+        C acc = cmul(ph[0], gk[0]);
+        for (int k = 1; k < p; ++k) acc = acc + cmul(ph[k * d], gk[k * d]);
+        Yb[i] = acc;
+    }
+    __syncthreads();
+    // ---- 5. DFT_d over nu; scatter to C[n][j] ----
+    C* Yd = fft_smem<T>(Yb, phi, A.rdd, q * c * q, d, sTwd);   // phi is dead: its buffer is scratch
+    C* Cn = Yd == sX ? sY : sX;
+    for (int i = tid; i < LQ; i += nt) {
+        const int np = i % d, t = i / d;              // destination n', source row t = (l c + r) q + u
+        const int u = t % q, lr = t / q;
+        const int r = lr % c, l = lr / c;
+        const int kappa = ((l - u) % q + q) % q;
+        const int off = l < u ? 1 : 0;
+        int tau = d - np - off;
+        if (tau >= d) tau -= d;
+        if (tau < 0) tau += d;
+        const int j = r + c * ((l * p) % q);
+        Cn[(kappa + q * np) * iM + j] = Yd[t * d + tau];
+    }
+    __syncthreads();
+    // ---- 6. DFT over j of the iN columns ----
+    C* X = fft_smem<T>(Cn, Yd, A.rdm, iN, iM, sTwm);
+    // ---- 7. output ----
+    C* out = (C*)A.B.out + w * A.B.M * A.B.N;
+    if (!freq) {
+        const C* __restrict__ E = (const C*)A.B.E;
+        const int Mi = (int)A.B.M, Ni = (int)A.B.N;
+        for (int i = tid; i < Mi * Ni; i += nt) {
+            const int n = i % Ni, mo = i / Ni;
+            int m = mo + __ldg(A.B.rot + n);
+            if (m >= Mi) m -= Mi;
+            out[i] = cmul(__ldg(E + n), X[n * iM + m]);
+        }
+    } else {
+        const unsigned long long Nr = (unsigned long long)A.B.Nr;
+        for (int i = tid; i < LQ; i += nt) {
+            const int kc = i % iM, n = i / iM;
+            const FbCol cc = fb_col(A.B, (unsigned long long)n);
+            const FbIter<C> it = fb_iter<C>(A.B, cc, kc ? Nr - (unsigned long long)kc : 0ull);
+            fb_put(A.B, out, it, X[i]);
+        }
+    }
+}

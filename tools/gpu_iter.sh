@@ -1,4 +1,4 @@
 set -x
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/t_it.log 2>&1; echo rc=$? >> gpurun_out/t_it.log
-timeout 300 python bench.py --config 4 --steps 20 > gpurun_out/b4_f.json 2>/dev/null
+timeout 900 python -m pytest tests/test_gpu_tiny.py -x -q > gpurun_out/t_tiny.log 2>&1; echo rc=$? >> gpurun_out/t_tiny.log
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/t_it.log 2>&1; echo rc=$? >> gpurun_out/t_it.log
 echo done
