@@ -38,4 +38,11 @@ template <typename V> __device__ __forceinline__ V mul_mi(V a) { V r; r.x = a.y;
 template <typename V> __device__ __forceinline__ V mul_pi(V a) { V r; r.x = -a.y; r.y = a.x; return r; }
 template <typename V, typename S> __device__ __forceinline__ V scale(V a, S s) { V r; r.x = a.x * s; r.y = a.y * s; return r; }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-serialisation
+// attribute may start while its predecessor in the stream drains; pdl_wait() returns once the
+// predecessor grid has completed and its memory is visible (a no-op without the attribute),
+// pdl_trigger() lets the successor launch as soon as every CTA of this grid has issued it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace nsdgt

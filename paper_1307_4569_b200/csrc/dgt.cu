@@ -204,6 +204,28 @@ __global__ void k_prechirp(cx<T>* out, const void* f, int real_in, const cx<T>* 
     }
 }
 
+// Launch with the programmatic-serialisation attribute (PDL; cplx.cuh pdl_wait / pdl_trigger):
+// the kernel's launch and prologue overlap its predecessor's tail.  NSDGT_PDL_OFF: plain launch.
+static bool pdl_enabled() {
+    static const bool on = std::getenv("NSDGT_PDL_OFF") == nullptr;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 struct ZakArgs {
     const void* f;     // [W][L] complex (or real) input of the inner separable DGT
     int real_in;
@@ -224,6 +246,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) zak_kernel(ZakArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
+    pdl_trigger();
+    pdl_wait();
     const int64_t d = A.d, p = A.p, q = A.q, c = A.c, L = A.L;
     const int RB = A.RB;
     const int nrb = (int)((c + RB - 1) / RB);
@@ -358,6 +382,23 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
     const int rblk = blockIdx.x % nrb, l = blockIdx.x / nrb;
     const int64_t w = blockIdx.y;
     const int r0 = rblk * RBC;
+    // d = 720 (one column per CTA, config 2): the window factors are loaded first, their
+    // latency under the gather and the first DFT (a plan table: before the PDL wait)
+    constexpr bool EG = D == 720;
+    C gv[NP];
+    pdl_trigger();
+    if constexpr (EG) {
+        const C* __restrict__ G = (const C*)A.G;
+#pragma unroll
+        for (int it = 0; it < NP; ++it) {
+            const int i = threadIdx.x + it * NT;
+            if (i < Q * RBC * D) {
+                const int u = i / (RBC * D), rem = i % (RBC * D);
+                gv[it] = __ldg(G + ((r0 + rem / D) * Q + u) * D + rem % D);
+            }
+        }
+    }
+    pdl_wait();
     C* R1 = (C*)smem_raw;
     C* R2 = R1 + Q * RBC * D;
     const C* __restrict__ tw = (const C*)A.tw;
@@ -398,13 +439,14 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
     C* Yb = phi == R1 ? R2 : R1;
     {
         const C* __restrict__ G = (const C*)A.G;
-        C gv[NP];
+        if constexpr (!EG) {
 #pragma unroll
-        for (int it = 0; it < NP; ++it) {
-            const int i = tid + it * NT;
-            if (i < Q * RBC * D) {
-                const int u = i / (RBC * D), rem = i % (RBC * D);
-                gv[it] = __ldg(G + ((r0 + rem / D) * Q + u) * D + rem % D);
+            for (int it = 0; it < NP; ++it) {
+                const int i = tid + it * NT;
+                if (i < Q * RBC * D) {
+                    const int u = i / (RBC * D), rem = i % (RBC * D);
+                    gv[it] = __ldg(G + ((r0 + rem / D) * Q + u) * D + rem % D);
+                }
             }
         }
 #pragma unroll
@@ -588,6 +630,7 @@ template <typename T, int IMCT = 0>
 __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
+    pdl_trigger();
     const int64_t iM = IMCT ? IMCT : A.iM, iN = A.iN, q = A.q, d = A.d;
     const int NT = A.NT;
     const int iMi = (int)iM, qi = (int)q, di = (int)d;
@@ -608,6 +651,18 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
         nt = (int)((iN - nb) < NT ? (iN - nb) : NT);
     }
     const int64_t w = blockIdx.y;
+    // T-branch with blockDim = 256 and nt | 256 (this tile's column count): thread t's output
+    // column is always nb + t mod nt, so its E(n) and rot(n) (plan tables) are loaded once,
+    // before the PDL wait
+    C Et = mk<T>(T(1), T(0));
+    int rott = 0;
+    const bool colfix = A.branch != DGT_BRANCH_FREQ && nt > 0 && 256 % nt == 0;
+    if (colfix) {
+        const int n = (int)nb + (int)(threadIdx.x % nt);
+        Et = __ldg((const C*)A.E + n);
+        rott = __ldg(A.rot + n);
+    }
+    pdl_wait();
     unsigned char* sbase = A.gscr ? A.gscr + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * A.gstride : smem_raw;
     C* bufA = (C*)sbase;
     C* bufB = bufA + (size_t)NT * iM;
@@ -616,7 +671,7 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
     // eight independent loads in flight per thread
     {
         const int total = nt * iMi, nbi = (int)nb, nsi = (int)ns;
-        constexpr int U = 8;
+        constexpr int U = IMCT > 0 ? 16 : 8;   // config 2 (NT = 16, M' = 200): all loads in one round
         for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
             C v[U];
 #pragma unroll
@@ -649,9 +704,9 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
             const int cl = i % nt;
             const int mo = i / nt;
             const int n = (int)nb + cl;
-            int m = mo + A.rot[n];
+            int m = mo + (colfix ? rott : A.rot[n]);
             if (m >= Mi) m -= Mi;
-            out[mo * Ni + n] = cmul(E[n], X[cl * iMi + m]);
+            out[mo * Ni + n] = cmul(colfix ? Et : E[n], X[cl * iMi + m]);
         }
     } else {
         C* out = (C*)A.out + w * A.M * A.N;
@@ -691,6 +746,8 @@ template <typename T, int MINB>
 __global__ void __launch_bounds__(256, MINB) out_f4096_kernel(OutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
+    pdl_trigger();
+    pdl_wait();
     C* S = (C*)smem_raw;
     const int tid = threadIdx.x;
     const int m = blockIdx.x;              // inner column
@@ -1556,8 +1613,8 @@ static int launch_front(Plan* P, const void* f, int64_t nb, cudaStream_t st) {
         FrontArgs FA{};
         FA.f = f; FA.real_in = real_in ? 1 : 0; FA.pre = P->pre; FA.H = P->fhat;
         FA.tw = P->tw_m; FA.twL = P->twL; FA.L = I.L;
-        front_f4096_kernel<T, 2 / kFrontRes, kFrontRes>
-            <<<dim3(180 / kFrontRes, (unsigned)nb), 256 * kFrontRes, front_smem(sizeof(C)), st>>>(FA);
+        CUDA_TRY(launch_pdl(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes>, dim3(180 / kFrontRes, (unsigned)nb),
+                            dim3(256 * kFrontRes), front_smem(sizeof(C)), st, FA));
         // a length-4096 DFT of 180 residues per signal (the DFT_180 runs in zak_rr0_kernel)
         prof_close(P, ph, PK_FRONTF, nb * L * ein, nb * 5.0 * L * 12.0, st);
         CUDA_TRY(cudaGetLastError());
@@ -1611,32 +1668,40 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);
     const int nrb = (int)((I.c + P->RB - 1) / P->RB);
     int ph = prof_open(P, st);
+    cudaError_t le;
     if (P->front)
-        zak_rr0_kernel<T, 8, kZrr0MinB><<<dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc), 128, zrr_smem<T>(), st>>>(A);
+        le = launch_pdl(zak_rr0_kernel<T, 8, kZrr0MinB>, dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc), dim3(128),
+                        zrr_smem<T>(), st, A);
     else if (P->zrr)
-        zak_rr_kernel<T, 8, kZrrMinB><<<dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc), 128, zrr_smem<T>(), st>>>(A);
+        le = launch_pdl(zak_rr_kernel<T, 8, kZrrMinB>, dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc), dim3(128),
+                        zrr_smem<T>(), st, A);
     else if (P->zsmall && sizeof(C) == 16)
-        zak_ct_kernel<T, 180, 4, 2, 128><<<dim3(2 * nrb * (unsigned)I.q, (unsigned)Wc), 128, P->smemA / 2, st>>>(A);
+        le = launch_pdl(zak_ct_kernel<T, 180, 4, 2, 128>, dim3(2 * nrb * (unsigned)I.q, (unsigned)Wc), dim3(128),
+                        P->smemA / 2, st, A);
     else if (P->zct == 180 && sizeof(C) == 16)
-        zak_ct_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+        le = launch_pdl(zak_ct_kernel<T, 180, 4, 4>, dim3(nrb * (unsigned)I.q, (unsigned)Wc), dim3(256), P->smemA, st, A);
     else if (P->zct == 180)
-        zak_ct_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+        le = launch_pdl(zak_ct_kernel<T, 180, 4, 8>, dim3(nrb * (unsigned)I.q, (unsigned)Wc), dim3(256), P->smemA, st, A);
     else if (P->zct == 720)
-        zak_ct_kernel<T, 720, 4, 1><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A);
+        le = launch_pdl(zak_ct_kernel<T, 720, 4, 1>, dim3(nrb * (unsigned)I.q, (unsigned)Wc), dim3(256), P->smemA, st, A);
     else
-        zak_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->gA ? 0 : P->smemA, st>>>(A);
+        le = launch_pdl(zak_kernel<T>, dim3(nrb * (unsigned)I.q, (unsigned)Wc), dim3(256), P->gA ? 0 : P->smemA, st, A);
+    CUDA_TRY(le);
     prof_close(P, ph, (P->zrr || P->front) ? PK_ZAKRR : P->zct ? PK_ZAKCT : PK_ZAK, by_in, fl_zak, st);
     const OutArgs B = make_out_args(P, P->Cws, c);
     const int ntiles = B.grouped ? (int)(I.q * ((I.d + P->NT - 1) / P->NT)) : (int)((I.iN + P->NT - 1) / P->NT);
     ph = prof_open(P, st);
     if (P->outk == 1)
-        out_f4096_kernel<T, 3><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+        le = launch_pdl(out_f4096_kernel<T, 3>, dim3((unsigned)I.iN, (unsigned)Wc), dim3(256), kOutF4096Elems * sizeof(C),
+                        st, B);
     else if (P->outk == 2)
-        out_f4096_kernel<T, 2><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+        le = launch_pdl(out_f4096_kernel<T, 2>, dim3((unsigned)I.iN, (unsigned)Wc), dim3(256), kOutF4096Elems * sizeof(C),
+                        st, B);
     else if (P->outct == 200)
-        out_kernel<T, 200><<<dim3(ntiles, (unsigned)Wc), 256, P->smemB, st>>>(B);
+        le = launch_pdl(out_kernel<T, 200>, dim3(ntiles, (unsigned)Wc), dim3(256), P->smemB, st, B);
     else
-        out_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->gB ? 0 : P->smemB, st>>>(B);
+        le = launch_pdl(out_kernel<T>, dim3(ntiles, (unsigned)Wc), dim3(256), P->gB ? 0 : P->smemB, st, B);
+    CUDA_TRY(le);
     prof_close(P, ph, P->outk ? PK_OUTF : PK_OUT, by_out, fl_out, st);
     CUDA_TRY(cudaGetLastError());
     return DGT_OK;
@@ -2053,7 +2118,7 @@ static int launch_tiny(Plan* P, const void* f, void* c, int64_t W, cudaStream_t 
         TinyArgs Tw = TA;
         Tw.f = (const char*)f + (size_t)w0 * I.L * (size_t)ein;
         Tw.B.out = (char*)c + (size_t)w0 * I.M * I.N * P->esz;
-        tiny_kernel<T><<<(unsigned)wc, 256, P->tiny_smem, st>>>(Tw);
+        CUDA_TRY(launch_pdl(tiny_kernel<T>, dim3((unsigned)wc), dim3(256), P->tiny_smem, st, Tw));
     }
     prof_close(P, ph, PK_TINY, W * (L * ein + MN * e) + L * e, fl, st);
     CUDA_TRY(cudaGetLastError());
@@ -2604,6 +2669,12 @@ void* dgt_debug_trace_log(dgt_plan_t plan) {
     Plan* P = (Plan*)plan;
     return P ? (void*)P->fp.tracelog : nullptr;
 }
+
+#ifdef NSDGT_TINY_TRACE
+int dgt_debug_tiny_trace(unsigned long long* out16) {   // experiment builds only
+    return cudaMemcpyFromSymbol(out16, g_tiny_trace, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 int64_t dgt_launches_per_execute(dgt_plan_t plan, int64_t W) {
     Plan* P = (Plan*)plan;

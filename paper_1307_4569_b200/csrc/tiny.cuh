@@ -38,6 +38,21 @@ __host__ __device__ inline int64_t tiny_elems(int64_t L, int64_t q, int64_t p, i
     return 2 * L + 2 * LX + L /* G */ + L /* chirp */ + (freq ? L : 0) /* twL */ + d + iM;
 }
 
+#ifdef NSDGT_TINY_TRACE
+// experiment builds only (tools): %globaltimer at the phase boundaries of block 0
+__device__ unsigned long long g_tiny_trace[16];
+#define TINY_MARK(k)                                                                            \
+    do {                                                                                        \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                              \
+            unsigned long long t_;                                                              \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+            g_tiny_trace[k] = t_;                                                               \
+        }                                                                                       \
+    } while (0)
+#else
+#define TINY_MARK(k) do { } while (0)
+#endif
+
 template <typename T>
 __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
     using C = cx<T>;
@@ -57,6 +72,8 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
     C* sTwm = sTwd + d;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int64_t w = blockIdx.x;
+    TINY_MARK(0);
+    pdl_trigger();
     // the output-stage tables go to L2 now (read once at the end)
     if (tid == 0) {
         const char* e = freq ? (const char*)A.B.ptab : (const char*)A.B.E;
@@ -70,20 +87,27 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
     {
         const C* __restrict__ pre = (const C*)A.pre;
         const C* __restrict__ chirp = (const C*)A.chirp;
+        // the plan's tables first (never written by a kernel of the stream), then -- once the
+        // predecessor grid is complete (PDL) -- the input, which a preceding kernel may produce
         for (int i = tid; i < L; i += nt) {
-            C v = A.real_in ? mk<T>(((const T*)A.f)[w * L + i], T(0)) : ((const C*)A.f)[w * L + i];
-            if (pre) v = cmul(v, __ldg(pre + i));
-            sF[i] = v;
             sG[i] = __ldg((const C*)A.G + i);
             sCh[i] = chirp ? __ldg(chirp + i) : mk<T>(T(1), T(0));
             if (freq) sTwL[i] = __ldg((const C*)A.twL + i);
         }
         for (int i = tid; i < d; i += nt) sTwd[i] = __ldg((const C*)A.twd + i);
         for (int i = tid; i < iM; i += nt) sTwm[i] = __ldg((const C*)A.twm + i);
+        pdl_wait();
+        for (int i = tid; i < L; i += nt) {
+            C v = A.real_in ? mk<T>(((const T*)A.f)[w * L + i], T(0)) : ((const C*)A.f)[w * L + i];
+            if (pre) v = cmul(v, __ldg(pre + i));
+            sF[i] = v;
+        }
     }
     __syncthreads();
+    TINY_MARK(1);
     // ---- 1. F-branch: f^ = DFT_L(f) ----
     const C* fh = freq ? fft_smem<T>(sF, sF2, A.rdL, 1, L, sTwL) : sF;
+    TINY_MARK(2);
     // ---- 2. Zak gather of all (l, r, k, s): sX[((l c + r) p + k) d + s] ----
     {
         const int Lc = L / c;
@@ -97,8 +121,10 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
         }
     }
     __syncthreads();
+    TINY_MARK(3);
     // ---- 3. DFT_d over s ----
     C* phi = fft_smem<T>(sX, sY, A.rdd, q * c * p, d, sTwd);
+    TINY_MARK(4);
     C* Yb = phi == sX ? sY : sX;
     // ---- 4. products Y(l, r, u; nu) at Yb[((l c + r) q + u) d + nu] ----
     for (int i = tid; i < LQ; i += nt) {
@@ -112,8 +138,10 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
         Yb[i] = acc;
     }
     __syncthreads();
+    TINY_MARK(5);
     // ---- 5. DFT_d over nu; scatter to C[n][j] ----
     C* Yd = fft_smem<T>(Yb, phi, A.rdd, q * c * q, d, sTwd);   // phi is dead: its buffer is scratch
+    TINY_MARK(6);
     C* Cn = Yd == sX ? sY : sX;
     for (int i = tid; i < LQ; i += nt) {
         const int np = i % d, t = i / d;              // destination n', source row t = (l c + r) q + u
@@ -128,8 +156,10 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
         Cn[(kappa + q * np) * iM + j] = Yd[t * d + tau];
     }
     __syncthreads();
+    TINY_MARK(7);
     // ---- 6. DFT over j of the iN columns ----
     C* X = fft_smem<T>(Cn, Yd, A.rdm, iN, iM, sTwm);
+    TINY_MARK(8);
     // ---- 7. output ----
     C* out = (C*)A.B.out + w * A.B.M * A.B.N;
     if (!freq) {
@@ -150,4 +180,6 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
             fb_put(A.B, out, it, X[i]);
         }
     }
+    __syncthreads();
+    TINY_MARK(9);
 }

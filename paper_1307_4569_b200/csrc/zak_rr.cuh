@@ -34,7 +34,7 @@ template <typename T> constexpr int zrr_smem() { return (180 + 2 * 8 * 180) * (i
 
 template <typename T, int RBC, int MINB>
 __global__ void __launch_bounds__(16 * RBC, MINB) zak_rr_kernel(ZakArgs A) {
-    constexpr int D = 180, Q = 4, NT = 16 * RBC;
+    constexpr int D = 180, Q = 4;
     using C = cx<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tws = (C*)smem_raw;              // W180^e, e < 180
@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(16 * RBC, MINB) zak_rr_kernel(ZakArgs A) {
     const int r0 = rblk * RBC;
     const int tid = threadIdx.x;
     const int rr = tid % RBC, hi = tid / RBC;   // hi: b (pass 15) or k1 (pass 12)
+    pdl_trigger();
+    pdl_wait();
     static_assert((12 * RBC) % 32 == 0, "the b-threads are whole warps (named barrier 1)");
     // ---- DFT 1, pass 1 (b-threads): gather v(12 a + b), a < 15, with the chirp; DFT_15 ----
     if (hi < 12) {
@@ -191,6 +193,8 @@ __global__ void __launch_bounds__(256 * RES, MINB) front_f4096_kernel(FrontArgs 
     const int r = blockIdx.x * RES + h;
     const int64_t w = blockIdx.y;
     const C* __restrict__ tw = (const C*)A.tw;
+    pdl_trigger();
+    pdl_wait();   // f may come from a preceding kernel; H may still be read by the previous Zak kernel
     C v[16];
     {
         const int64_t base = w * A.L + r;
@@ -260,6 +264,8 @@ __global__ void __launch_bounds__(16 * RBC, MINB) zak_rr0_kernel(ZakArgs A) {
     const int tid = threadIdx.x;
     const int rr = tid % RBC, hi = tid / RBC;
     const int x = r0 + rr + c * l;            // column of H / f^ (x < 4096)
+    pdl_trigger();
+    pdl_wait();
     // ---- stage 0, pass 1 (b-threads): H(12 a + b, x), DFT_15 over a ----
     if (hi < 12) {
         const int b = hi;
