@@ -587,7 +587,7 @@ __device__ __forceinline__ void fb_step(const OutArgs& A, FbIter<C>& it) {
     if (!A.C3) it.ph = cmul(it.ph, it.dph);
 }
 template <typename C>
-__device__ __forceinline__ void fb_put(const OutArgs& A, C* out, const FbIter<C>& it, C val) {
+__device__ __forceinline__ void fb_dest(const OutArgs& A, const FbIter<C>& it, size_t* dst, C* phase) {
     const unsigned int twoN = (unsigned int)(2 * A.N), Nn = (unsigned int)A.N;
     C ph;
     if (A.C3) {
@@ -604,7 +604,15 @@ __device__ __forceinline__ void fb_put(const OutArgs& A, C* out, const FbIter<C>
     unsigned int r = it.xx - kt * bu;
     if (r >= bu) { r -= bu; ++kt; }
     if (r >= bu) ++kt;
-    out[(size_t)kt * Nn + mt] = cmul(ph, val);
+    *dst = (size_t)kt * Nn + mt;
+    *phase = ph;
+}
+template <typename C>
+__device__ __forceinline__ void fb_put(const OutArgs& A, C* out, const FbIter<C>& it, C val) {
+    size_t dst;
+    C ph;
+    fb_dest(A, it, &dst, &ph);
+    out[dst] = cmul(ph, val);
 }
 // column m, coefficients kc = kc0 + 256 i, i < cnt (kc0 < 256; CNT > 0: compile-time count,
 // fully unrolled so get(i) may index registers)
@@ -1370,6 +1378,10 @@ struct Plan {
     int zrr = 0;             // forward Zak with zak_rr_kernel (d = 180 = 12 x 15 in registers)
     int front = 0;           // F-branch front end by front_f4096_kernel + zak_rr0_kernel (L = 180 x 4096)
     int tiny = 0;            // whole transform of a signal in one CTA (tiny.cuh)
+    unsigned int* tiny_dst = nullptr;   // F-branch output remap table (tiny.cuh)
+    void* tiny_ph = nullptr;
+    void* tiny_pack = nullptr;          // the one-CTA path's tables in one allocation (TinyArgs)
+    TinyArgs tiny_args{};
     size_t tiny_smem = 0;
     Radices rd_L{};
     void* twL = nullptr;     // W_L^e, e < 180 * 256 (front_f4096_kernel)
@@ -1441,7 +1453,7 @@ static void free_plan(Plan* P) {
     if (P->inv_alias & 2) P->finv = nullptr;
     void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
                     P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv, P->gt64,
-                    P->scrA, P->scrB, P->twL};
+                    P->scrA, P->scrB, P->twL, P->tiny_dst, P->tiny_ph, P->tiny_pack};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     free_fast(&P->fp);
@@ -1507,6 +1519,8 @@ static int exec_fft(Plan* P, const void* in, void* out, int64_t nb, int dir, cud
     return DGT_OK;
 }
 
+static OutArgs make_out_args(const Plan* P, void* Cbuf, void* c);
+
 template <typename T>
 static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st) {
     using C = cx<T>;
@@ -1562,6 +1576,36 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
     } else {
         CUDA_TRY(cudaMalloc(&P->ptab, sizeof(C) * 2 * I.N));
         k_phase_table<T><<<grid_for(2 * I.N), 256, 0, st>>>((C*)P->ptab, I.N);
+    }
+    if (P->tiny && I.branch == DGT_BRANCH_FREQ) {   // the one-CTA path's output remap table
+        const int64_t n = I.iM * I.iN;
+        CUDA_TRY(cudaMalloc(&P->tiny_dst, sizeof(unsigned int) * n));
+        CUDA_TRY(cudaMalloc(&P->tiny_ph, sizeof(C) * n));
+        const OutArgs B = make_out_args(P, nullptr, nullptr);
+        k_tiny_remap<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B, P->tiny_dst, (C*)P->tiny_ph, (int)I.iM, (int)I.iN);
+    }
+    if (P->tiny) {
+        // every table the one-CTA kernel reads, copied into one allocation: after the L2 flush
+        // of a latency measurement each separate allocation costs its own cold page walk
+        const bool freq = I.branch == DGT_BRANCH_FREQ;
+        const int64_t LQ = I.iM * I.iN;
+        struct Part { const void* src; size_t bytes; const void** dst; };
+        TinyArgs& TA = P->tiny_args;
+        std::vector<Part> parts = {{P->G, sizeof(C) * L, &TA.G}, {P->chirp, P->chirp ? sizeof(C) * L : 0, &TA.chirp},
+                                   {P->twL, freq ? sizeof(C) * L : 0, &TA.twL}, {P->tw_d, sizeof(C) * I.d, &TA.twd},
+                                   {P->tw_m, sizeof(C) * I.iM, &TA.twm}, {P->tiny_ph, freq ? sizeof(C) * LQ : 0, &TA.oph},
+                                   {P->tiny_dst, freq ? sizeof(unsigned int) * LQ : 0, &TA.odst},
+                                   {P->pre, P->pre ? sizeof(C) * L : 0, &TA.pre}};
+        size_t tot = 0;
+        for (auto& pt : parts) tot += (pt.bytes + 255) / 256 * 256;
+        CUDA_TRY(cudaMalloc(&P->tiny_pack, tot));
+        size_t off = 0;
+        for (auto& pt : parts) {
+            if (!pt.bytes) { *pt.dst = nullptr; continue; }
+            CUDA_TRY(cudaMemcpyAsync((char*)P->tiny_pack + off, pt.src, pt.bytes, cudaMemcpyDeviceToDevice, st));
+            *pt.dst = (char*)P->tiny_pack + off;
+            off += (pt.bytes + 255) / 256 * 256;
+        }
     }
     CUDA_TRY(cudaGetLastError());
     int rc = build_fast<T>(&P->fp, P->info, gt, P->E, (P->flags & DGT_FORCE_GENERIC) != 0, st);
@@ -1826,12 +1870,12 @@ static int configure(Plan* P, int64_t max_chunk) {
     CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kOutF4096Elems * e)));
     // short signals: the whole transform of a signal in one CTA when its tables and buffers fit
-    // 96 KB of shared memory (config 1); NSDGT_TINY_OFF keeps the chunked kernels
+    // 160 KB of shared memory (config 1); NSDGT_TINY_OFF keeps the chunked kernels
     {
         const bool freq = I.branch == DGT_BRANCH_FREQ;
         const int64_t te = tiny_elems(I.L, I.q, I.p, I.d, I.iM, freq);
         const Radices rl = make_radices((int)std::min<int64_t>(I.L, 1 << 30));
-        P->tiny = (!std::getenv("NSDGT_TINY_OFF") && te * (int64_t)e <= 96 * 1024 && I.iM * I.iN == I.L / I.p * I.q &&
+        P->tiny = (!std::getenv("NSDGT_TINY_OFF") && te * (int64_t)e <= 160 * 1024 && I.iM * I.iN == I.L / I.p * I.q &&
                    I.iM == I.c * I.q && rl.nst <= kMaxStages) ? 1 : 0;
         if (P->tiny) {
             P->rd_L = rl;
@@ -2100,9 +2144,8 @@ static int execute_mw(Plan* P, const void* f, void* c, int64_t W, cudaStream_t s
 template <typename T>
 static int launch_tiny(Plan* P, const void* f, void* c, int64_t W, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
-    TinyArgs TA{};
-    TA.f = f; TA.real_in = (P->flags & DGT_REAL_INPUT) ? 1 : 0; TA.pre = P->pre; TA.chirp = P->chirp; TA.G = P->G;
-    TA.twL = P->twL; TA.twd = P->tw_d; TA.twm = P->tw_m;
+    TinyArgs TA = P->tiny_args;   // table pointers into P->tiny_pack (build_tables)
+    TA.f = f; TA.real_in = (P->flags & DGT_REAL_INPUT) ? 1 : 0;
     TA.rdL = P->rd_L; TA.rdd = P->rd_d; TA.rdm = P->rd_m;
     TA.L = (int)I.L; TA.c = (int)I.c; TA.d = (int)I.d; TA.p = (int)I.p; TA.q = (int)I.q;
     TA.iM = (int)I.iM; TA.iN = (int)I.iN;

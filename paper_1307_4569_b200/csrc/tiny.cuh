@@ -26,16 +26,36 @@ struct TinyArgs {
     const void* twL;      // W_L^k, k < L (F-branch)
     const void* twd;      // W_d^k
     const void* twm;      // W_iM^k
+    const void* odst;           // F-branch: destination c index (uint32) of X[n iM + kc] (plan table)
+    const void* oph;            // F-branch: its Alg. 1 phase
     Radices rdL, rdd, rdm;
     int L, c, d, p, q, iM, iN;
     OutArgs B;            // output constants (out, M, N, E / rot or the F-branch remap)
 };
 
+// Plan time (F-branch): the output remap of every X[n iM + kc] -- destination index and phase,
+// the same residues fb_column computes per coefficient (fb_col, fb_iter, fb_dest).
+template <typename T>
+__global__ void k_tiny_remap(OutArgs B, unsigned int* odst, cx<T>* oph, int iM, int iN) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= iM * iN) return;
+    const int kc = i % iM, n = i / iM;
+    const FbCol cc = fb_col(B, (unsigned long long)n);
+    const FbIter<cx<T>> it = fb_iter<cx<T>>(B, cc, kc ? (unsigned long long)B.Nr - (unsigned long long)kc : 0ull);
+    size_t dst;
+    cx<T> ph;
+    fb_dest(B, it, &dst, &ph);
+    odst[i] = (unsigned int)dst;
+    oph[i] = ph;
+}
+
 // shared-memory elements of tiny_kernel (also the host's fit test)
 __host__ __device__ inline int64_t tiny_elems(int64_t L, int64_t q, int64_t p, int64_t d, int64_t iM, bool freq) {
     const int64_t LQ = L * q / p;   // products / intermediate (= iM iN)
     const int64_t LX = LQ > L ? LQ : L;   // work buffers: the Zak gather (L) and the products (LQ)
-    return 2 * L + 2 * LX + L /* G */ + L /* chirp */ + (freq ? L : 0) /* twL */ + d + iM;
+    // + F-branch: W_L, the output phases (LQ) and destinations (LQ x 4 bytes, counted as LQ / 2
+    //   16-byte or LQ / 2 8-byte elements rounded up)
+    return 2 * L + 2 * LX + L /* G */ + L /* chirp */ + (freq ? L + LQ + (LQ + 1) / 2 : 0) + d + iM;
 }
 
 #ifdef NSDGT_TINY_TRACE
@@ -54,7 +74,7 @@ __device__ unsigned long long g_tiny_trace[16];
 #endif
 
 template <typename T>
-__global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
+__global__ void __launch_bounds__(256) tiny_kernel(const __grid_constant__ TinyArgs A) {
     using C = cx<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int L = A.L, c = A.c, d = A.d, p = A.p, q = A.q, iM = A.iM, iN = A.iN;
@@ -68,7 +88,9 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
     C* sG = sY + LX;             // L
     C* sCh = sG + L;             // L
     C* sTwL = sCh + L;           // L (F-branch)
-    C* sTwd = sTwL + (freq ? L : 0);
+    C* sPh = sTwL + (freq ? L : 0);            // LQ (F-branch)
+    unsigned int* sDst = (unsigned int*)(sPh + (freq ? LQ : 0));   // LQ (F-branch)
+    C* sTwd = (C*)((char*)sPh + (freq ? (int64_t)LQ * sizeof(C) + (LQ + 1) / 2 * sizeof(C) : 0));
     C* sTwm = sTwd + d;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int64_t w = blockIdx.x;
@@ -96,6 +118,12 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
         }
         for (int i = tid; i < d; i += nt) sTwd[i] = __ldg((const C*)A.twd + i);
         for (int i = tid; i < iM; i += nt) sTwm[i] = __ldg((const C*)A.twm + i);
+        if (freq && A.odst) {
+            for (int i = tid; i < LQ; i += nt) {
+                sPh[i] = __ldg((const C*)A.oph + i);
+                sDst[i] = __ldg((const unsigned int*)A.odst + i);
+            }
+        }
         pdl_wait();
         for (int i = tid; i < L; i += nt) {
             C v = A.real_in ? mk<T>(((const T*)A.f)[w * L + i], T(0)) : ((const C*)A.f)[w * L + i];
@@ -171,6 +199,8 @@ __global__ void __launch_bounds__(256) tiny_kernel(TinyArgs A) {
             if (m >= Mi) m -= Mi;
             out[i] = cmul(__ldg(E + n), X[n * iM + m]);
         }
+    } else if (A.odst) {
+        for (int i = tid; i < LQ; i += nt) out[sDst[i]] = cmul(sPh[i], X[i]);
     } else {
         const unsigned long long Nr = (unsigned long long)A.B.Nr;
         for (int i = tid; i < LQ; i += nt) {
