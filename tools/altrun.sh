@@ -3,7 +3,7 @@
 set -e
 lib=$(realpath "$1"); shift
 tmp=$(mktemp -d)
-cp -r paper_1307_4569_b200 synthetic tools oracle bench.py $tmp/
+cp -r paper_1307_4569_b200 synthetic tools oracle tests bench.py $tmp/
 cp "$lib" $tmp/paper_1307_4569_b200/libnsdgt.so
 touch -d '+1 hour' $tmp/paper_1307_4569_b200/libnsdgt.so
 cd $tmp && python "$@"
