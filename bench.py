@@ -343,7 +343,8 @@ def main():
     # SURVEY 8(d) algorithmic bytes of this rank's step; a step that moves less than ~4x the
     # 126 MB L2 could be served from L2 across iterations, so then L2 is flushed (a 512 MB
     # memset) between steps, outside per-step event pairs, and the step times are summed
-    step_bytes = Wr * (wl.L * (8 if wl.dtype == "c64" else 16) // (2 if wl.real_input else 1)
+    # (synthesis writes complex signals even for real-input plans)
+    step_bytes = Wr * (wl.L * (8 if wl.dtype == "c64" else 16) // (2 if wl.real_input and not args.inverse else 1)
                        + wl.M * wl.N * (8 if wl.dtype == "c64" else 16)) + wl.L * (8 if wl.dtype == "c64" else 16)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if step_bytes <= 4 * 126e6 else None
     e0 = torch.cuda.Event(enable_timing=True)
