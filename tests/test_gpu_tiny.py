@@ -76,3 +76,32 @@ def test_tiny_many_signals_and_empty(env):
     for w in (0, 1777, 2999):
         assert torch.equal(c[w], plan.execute(ft[w:w + 1])[0])
     assert rel(c[1777].cpu().numpy(), oracle.dgt(f[1777], g, a, M, l1, l2)) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 3])
+def test_input_produced_by_preceding_kernel(env, cfg):
+    """The chunk kernels, front_f4096 and the one-CTA kernel are launched with programmatic
+    dependent launch; each must wait for the preceding grid before reading the caller's input
+    or writing anything.  Here a torch kernel writes f on the same stream right before every
+    execute (and another reads the output right after): the results equal a fully
+    synchronised run, repeated so that a missing wait would show."""
+    torch, nsdgt, oracle = env
+    wl = CONFIGS[cfg]
+    g = window(wl)
+    f0 = torch.from_numpy(batch(wl, 0, min(wl.W, 4))).cuda()
+    plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, real_input=wl.real_input)
+    ref = []
+    for k in range(3):
+        fk = f0 * (k + 1) - 0.5 * k
+        torch.cuda.synchronize()
+        ref.append(plan.execute(fk).clone())
+        torch.cuda.synchronize()
+    fbuf = torch.empty_like(f0)
+    out = torch.empty_like(ref[0])
+    for rep in range(4):
+        for k in range(3):
+            torch.mul(f0, k + 1, out=fbuf)
+            fbuf.sub_(0.5 * k)                   # f written by kernels right before the execute
+            plan.execute(fbuf, out=out)
+            got = out.clone()                    # read right after, same stream
+            assert torch.equal(got, ref[k]), (rep, k)
