@@ -1853,6 +1853,10 @@ static int configure(Plan* P, int64_t max_chunk) {
         CUDA_TRY(cudaFuncSetAttribute(zak_rr0_kernel<T, 8, kZrr0MinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zrr_smem<T>()));
         CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem((int)e)));
+        CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem((int)e)));
+        CUDA_TRY(cudaFuncSetAttribute(zak_rr0_adj_kernel<T, 8, kZrr0MinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      zrr_smem<T>()));
     }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     // compile-time output DFT for M' = 200 (config 2, time shear)
@@ -2000,7 +2004,10 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     void* zout = freq ? spectra : f;
     const double lg_d = std::log2((double)I.d);
     ph = prof_open(P, st);
-    if (P->zct == 180 && sizeof(C) == 16)
+    if (P->front)   // config 4: the register-resident adjoint, h(r, x) for front_f4096<..., ADJ>
+        CUDA_TRY(launch_pdl(zak_rr0_adj_kernel<T, 8, kZrr0MinB>, dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc),
+                            dim3(128), zrr_smem<T>(), st, A, zout));
+    else if (P->zct == 180 && sizeof(C) == 16)
         zak_ct_adj_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
     else if (P->zct == 180)
         zak_ct_adj_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
@@ -2021,6 +2028,15 @@ static int launch_inverse_tail(Plan* P, void* f, int64_t nb, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
     const double e = (double)sizeof(C), L = (double)I.L;
     const int ph = prof_open(P, st);
+    if (P->front) {   // the adjoint of front_f4096 (4096-point DFTs per residue, stride-180 writes)
+        FrontArgs FA{};
+        FA.f = P->finv; FA.real_in = 0; FA.pre = P->pre; FA.H = f; FA.tw = P->tw_m; FA.twL = P->twL; FA.L = I.L;
+        CUDA_TRY(launch_pdl(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes, true>, dim3(180 / kFrontRes, (unsigned)nb),
+                            dim3(256 * kFrontRes), front_smem(sizeof(C)), st, FA));
+        prof_close(P, ph, PK_FRONTF, nb * L * e, nb * 5.0 * L * 12.0, st);
+        CUDA_TRY(cudaGetLastError());
+        return DGT_OK;
+    }
     void* dst = P->pre ? P->finv : f;
     int rc = exec_fft(P, P->finv, dst, nb, CUFFT_INVERSE, st);
     if (rc) return rc;

@@ -183,7 +183,11 @@ __device__ __forceinline__ void twiddle16(C* v, C w1) {
 // RES samples f(180 q + r0 + h) of a lane pair are adjacent (RES = 2: 32-byte sectors used
 // whole instead of half), each residue has its own exchange buffer (offset by 4 elements so the
 // two halves of a quarter warp hit different banks).
-template <typename T, int MINB, int RES>
+// ADJ (synthesis, the adjoint of the front end): input h(r, x) = conj(H'(r, x)) as written by
+// zak_rr0_adj_kernel, contiguous in x; the W_L^{r x} twiddle on load, the same three passes
+// (now over x -> q) and f(180 q + r) = conj(X(q)) conj(pchirp(L, s1)) stored at stride 180
+// (the unnormalised inverse DFT of Alg. 1 line 23's FFT, as conj(DFT(conj(.)))).
+template <typename T, int MINB, int RES, bool ADJ = false>
 __global__ void __launch_bounds__(256 * RES, MINB) front_f4096_kernel(FrontArgs A) {
     using C = cx<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -196,7 +200,12 @@ __global__ void __launch_bounds__(256 * RES, MINB) front_f4096_kernel(FrontArgs 
     pdl_trigger();
     pdl_wait();   // f may come from a preceding kernel; H may still be read by the previous Zak kernel
     C v[16];
-    {
+    if constexpr (ADJ) {
+        const C* hr = (const C*)A.f + w * A.L + (int64_t)r * 4096;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = hr[tid + 256 * i];
+        twiddle16b(v, __ldg((const C*)A.twL + r * tid), __ldg((const C*)A.twL + 256 * r));
+    } else {
         const int64_t base = w * A.L + r;
         const C* __restrict__ pre = (const C*)A.pre;
 #pragma unroll
@@ -232,6 +241,19 @@ __global__ void __launch_bounds__(256 * RES, MINB) front_f4096_kernel(FrontArgs 
 #pragma unroll
     for (int q0 = 0; q0 < 16; ++q0) v[q0] = S[tid * 17 + q0];
     dft16<T>(v);
+    if constexpr (ADJ) {
+        // f(180 (tid + 256 k) + r) = conj(X) conj(pre): lane pairs (h = 0, 1) write 32 bytes
+        const C* __restrict__ pre = (const C*)A.pre;
+        C* fo = (C*)A.H + w * A.L + r;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int l = 180 * (tid + 256 * k);
+            C y = mk<T>(v[k].x, -v[k].y);
+            if (pre) y = cmulc(y, __ldg(pre + r + l));
+            fo[l] = y;
+        }
+        return;
+    }
     // H(r, x) = W_L^{r x} X(x), x = tid + 256 x2: W_L^{r tid} (W_L^{256 r})^{x2}
     twiddle16b(v, __ldg((const C*)A.twL + r * tid), __ldg((const C*)A.twL + 256 * r));
     C* H = (C*)A.H + w * A.L + (int64_t)r * 4096;
@@ -342,5 +364,111 @@ __global__ void __launch_bounds__(16 * RBC, MINB) zak_rr0_kernel(ZakArgs A) {
                 else Cw[((jbase + rr) * Q + kappa) * D + np] = z[k];
             }
         }
+    }
+}
+
+// Adjoint of zak_rr0_kernel (synthesis, config 4): C' [n][j] -> h(r, x) = conj(H'(r, x)), kept
+// conjugated so that every DFT is a forward one (conj(DFT^H(y)) = DFT(conj y)):
+//   S2 per u, tau = p + 15 k -> nu = t + 12 e: gather conj(T'_u(tau)) through the forward
+//      scatter map, p-thread DFT_12 over k, W180^{p t}, exchange, t-thread DFT_15 over p;
+//      acc(nu) += y_u(nu) G_u(nu) in the t-thread's registers (= conj(Phi'(nu)))
+//   S1 nu = t + 12 e -> j = p + 15 k: t-thread DFT_15 over e, W180^{t p}, exchange, p-thread
+//      DFT_12 over t; times the chirp P_{-s0}(x + 4096 j)  (= conj of the adjoint's value)
+//   S0 j = p + 15 k -> r = b + 12 a: p-thread DFT_12 over k, W180^{p b}, exchange, b-thread
+//      DFT_15 over p; h(b + 12 a, x) stored [w][r][x] for front_f4096_kernel<..., ADJ>.
+template <typename T, int RBC, int MINB>
+__global__ void __launch_bounds__(16 * RBC, MINB) zak_rr0_adj_kernel(ZakArgs A, void* hout) {
+    constexpr int D = 180, Q = 4;
+    using C = cx<T>;
+    static_assert((12 * RBC) % 32 == 0, "the 12-lane groups are whole warps");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* tws = (C*)smem_raw;
+    C* X0 = tws + D;
+    C* X1 = X0 + RBC * D;
+    const int c = (int)A.c;
+    const int nrb = c / RBC;
+    const int rblk = blockIdx.x % nrb, l = blockIdx.x / nrb;
+    const int64_t w = blockIdx.y;
+    const int r0 = rblk * RBC;
+    const int tid = threadIdx.x;
+    const int rr = tid % RBC, hi = tid / RBC;
+    const int x = r0 + rr + c * l;
+    pdl_trigger();
+    for (int i = tid; i < D; i += 16 * RBC) tws[i] = ((const C*)A.tw)[i];
+    pdl_wait();
+    __syncthreads();
+    const C* __restrict__ G = (const C*)A.G + (int64_t)(r0 + rr) * Q * D;
+    const C* Cw = (const C*)A.C + w * A.iM * Q * D;
+    const int jbase = r0 + c * (l % Q);
+    const int iM = (int)A.iM;
+    C acc[15];
+#pragma unroll
+    for (int e = 0; e < 15; ++e) acc[e] = mk<T>(T(0), T(0));
+#pragma unroll 1
+    for (int u = 0; u < Q; ++u) {
+        C* Xu = (u & 1) ? X1 : X0;
+        if (hi < 15) {
+            const int p = hi;
+            const int kappa = (l - u + Q) % Q;
+            const int off = l < u ? 1 : 0;
+            C z[12];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) {
+                const int tau = p + 15 * k;
+                int np = D - tau - off;
+                if (np >= D) np -= D;
+                if (np < 0) np += D;
+                const C v = A.cnj ? Cw[(int64_t)(kappa + Q * np) * iM + jbase + rr] : Cw[((jbase + rr) * Q + kappa) * D + np];
+                z[k] = mk<T>(v.x, -v.y);
+            }
+            dft_pq<T, 4, 3, 180>(z, 15);   // over k -> t
+#pragma unroll
+            for (int t = 0; t < 12; ++t) Xu[(p * 12 + t) * RBC + rr] = t ? cmul(z[t], tws[p * t]) : z[t];
+        }
+        __syncthreads();
+        if (hi < 12) {
+            const int t = hi;
+            C y[15];
+#pragma unroll
+            for (int p = 0; p < 15; ++p) y[p] = Xu[(p * 12 + t) * RBC + rr];
+            dft_pq<T, 3, 5, 180>(y, 12);   // over p -> e: y_u(t + 12 e)
+#pragma unroll
+            for (int e = 0; e < 15; ++e) acc[e] = acc[e] + cmul(y[e], __ldg(G + u * D + t + 12 * e));
+        }
+    }
+    // ---- S1: acc(t + 12 e) -> j = p + 15 k (X0 was last read in u = 2, before u = 3's barrier) ----
+    if (hi < 12) {
+        const int t = hi;
+        dft_pq<T, 3, 5, 180>(acc, 12);     // over e -> p
+#pragma unroll
+        for (int p = 0; p < 15; ++p) X0[(t * 15 + p) * RBC + rr] = p ? cmul(acc[p], tws[t * p]) : acc[p];
+    }
+    __syncthreads();
+    if (hi < 15) {
+        const int p = hi;
+        C e2[12];
+#pragma unroll
+        for (int t = 0; t < 12; ++t) e2[t] = X0[(t * 15 + p) * RBC + rr];
+        dft_pq<T, 4, 3, 180>(e2, 15);      // over t -> k: j = p + 15 k
+        const C* __restrict__ chirp = (const C*)A.chirp;
+        if (chirp) {
+#pragma unroll
+            for (int k = 0; k < 12; ++k) e2[k] = cmul(e2[k], __ldg(chirp + x + 4096 * (p + 15 * k)));
+        }
+        // ---- S0: j = p + 15 k -> r = b + 12 a ----
+        dft_pq<T, 4, 3, 180>(e2, 15);      // over k -> b
+#pragma unroll
+        for (int b = 0; b < 12; ++b) X1[(p * 12 + b) * RBC + rr] = b ? cmul(e2[b], tws[p * b]) : e2[b];
+    }
+    __syncthreads();
+    if (hi < 12) {
+        const int b = hi;
+        C hv[15];
+#pragma unroll
+        for (int p = 0; p < 15; ++p) hv[p] = X1[(p * 12 + b) * RBC + rr];
+        dft_pq<T, 3, 5, 180>(hv, 12);      // over p -> a: r = b + 12 a
+        C* Ho = (C*)hout + w * A.L + (int64_t)b * 4096 + x;
+#pragma unroll
+        for (int a = 0; a < 15; ++a) Ho[a * 12 * 4096] = hv[a];
     }
 }

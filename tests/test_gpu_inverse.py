@@ -184,8 +184,9 @@ def test_fused_synthesis_matches_generic_and_oracle(torch_cuda, nsdgt, oracle_mo
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_config4_synthesis_kernels_match_generic(torch_cuda, nsdgt, dtype, monkeypatch):
-    """Config 4's synthesis kernels (zak_ct_adj_kernel, out_f4096_adj_kernel) against the generic
-    adjoint kernels (selected at plan time by NSDGT_ZAK_RT / NSDGT_OUT_GENERIC)."""
+    """Config 4's synthesis kernels (out_f4096_adj_kernel, zak_rr0_adj_kernel and the adjoint
+    front_f4096 -- no cuFFT) against the generic adjoint kernels with cuFFT (selected at plan
+    time by NSDGT_ZAK_RT / NSDGT_OUT_GENERIC, which also drop the front path)."""
     torch = torch_cuda
     wl = CONFIGS[3]
     g = window(wl)
@@ -198,3 +199,22 @@ def test_config4_synthesis_kernels_match_generic(torch_cuda, nsdgt, dtype, monke
     pg = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
     fg = pg.inverse(c).cpu().numpy()
     assert rel(ff, fg) <= TOL[dtype]
+
+
+def test_config4_lattice_prechirp_synthesis(torch_cuda, nsdgt, oracle_mod):
+    """The adjoint front_f4096 with its conj(pchirp(L, s1)) factor: config 4's lattice at
+    lambda = 1/6 (s1 = 128, on the front path), one signal of random coefficients in full
+    against the oracle's idgt."""
+    torch = torch_cuda
+    wl = CONFIGS[3]
+    info = nsdgt.lattice_plan(wl.L, wl.a, wl.M, 1, 6)
+    assert info["pre_sigma"] != 0 and info["d"] == 180
+    g = window(wl)
+    rng = np.random.default_rng(13)
+    c = rand_c(rng, 1, wl.M, wl.L // wl.a, "c128")
+    plan = nsdgt.Plan(wl.L, wl.a, wl.M, 1, 6, g, dtype="c128")
+    plan.profile_begin()
+    f = plan.inverse(torch.from_numpy(c).cuda()).cpu().numpy()
+    assert "front_f4096" in {k["name"] for k in plan.profile_end()}
+    ref = oracle_mod.idgt(c, g, wl.a, wl.M, 1, 6)
+    assert rel(f, ref) <= TOL["c128"]

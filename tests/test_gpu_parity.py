@@ -211,7 +211,8 @@ def test_config4_front_and_zak_variants_agree(torch_cuda, nsdgt, oracle_mod, dty
     """Config 4 runs front_f4096 + zak_rr0 (the length-L FFT split as 4096-point DFTs of the
     180 residues and a DFT_180 inside the Zak kernel; no cuFFT).  The same plan with cuFFT's
     front end + zak_rr (NSDGT_FRONT_CUFFT) and with cuFFT + the Stockham zak_ct (also
-    NSDGT_ZAK_CT) agree with it and with the oracle on sampled columns."""
+    NSDGT_ZAK_CT) agree with it and with the oracle on sampled columns; the synthesis
+    (zak_rr0_adj + the adjoint front) agrees with cuFFT + zak_ct_adj."""
     torch = torch_cuda
     wl = CONFIGS[3]
     g = window(wl)
@@ -222,13 +223,18 @@ def test_config4_front_and_zak_variants_agree(torch_cuda, nsdgt, oracle_mod, dty
     c = p.execute(f)
     names = {k["name"] for k in p.profile_end()}
     assert "front_f4096" in names and "front_fft_cufft" not in names, names
+    # synthesis: zak_rr0_adj + the adjoint front_f4096 (no cuFFT) against cuFFT + zak_ct_adj
+    rsyn = p.inverse(c)
     monkeypatch.setenv("NSDGT_FRONT_CUFFT", "1")
-    c1 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype).execute(f)
+    p1 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype)
+    c1 = p1.execute(f)
+    rsyn1 = p1.inverse(c)
     monkeypatch.setenv("NSDGT_ZAK_CT", "1")
     c2 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=dtype).execute(f)
     tol = TOL[dtype]
     assert rel(c.cpu().numpy(), c1.cpu().numpy()) <= tol
     assert rel(c.cpu().numpy(), c2.cpu().numpy()) <= tol
+    assert rel(rsyn.cpu().numpy(), rsyn1.cpu().numpy()) <= tol
     cols = np.sort(np.random.default_rng(45).choice(wl.N, 16, replace=False))
     ref = oracle_mod.dgt(fnp, g, wl.a, wl.M, wl.lam1, wl.lam2, cols=cols)
     assert rel(c[:, :, torch.from_numpy(cols).cuda()].cpu().numpy(), ref) <= tol
