@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(128, MINB) fused7_kernel(Args A, const __grid_
     auto load_ring = [&](int slot, int line, int bt, int b) {   // slot = w mod S
         const float2* src = A.ws + (int64_t)slot * MQD + (int64_t)h8 * (Q * D) + line * 16 + 8 * bt + s8;
 #pragma unroll
-#ifdef NSDGT_XP_NOFR
+#if defined(NSDGT_XP_NOFR) || defined(NSDGT_XP_NORING)   // experiment builds only: no ring loads
         for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = make_float2((float)k, (float)(line + slot));
 #else
         for (int k = 16 * b; k < 16 * b + 16 && k < R1; ++k) pre[k] = ld_cg(src + (int64_t)(16 * k) * (Q * D));
