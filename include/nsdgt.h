@@ -8,7 +8,10 @@
  *   Computed by the shear algorithm, Algorithm 1 of PAPER.md:852-900 (Sec. 4.1),
  *   with the frequency-domain trick of PAPER.md:902-919 and a Zak/factorization
  *   separable DGT (Eq. rect-flops) on hand-written sm_100a kernels;
- *   cuFFT is used only for the length-L FFTs of the frequency-shear branch.
+ *   cuFFT is used only for the length-L FFTs of the frequency-shear branch, except where
+ *   L = 180 x 4096 = d x (c q) (BASELINE config 4), whose length-L FFT and its adjoint run
+ *   in the library's own kernels, and on the one-CTA path for short signals (DGT_ECUFFT
+ *   cannot occur there).
  *
  * Conventions for every entry point:
  *   - Return value: a dgt_status (0 = DGT_OK).  A failed dgt_plan never returns a plan.
@@ -24,6 +27,9 @@
  *     executed concurrently from two streams (its workspace is shared).
  *   - Output is bitwise deterministic for a given (plan, f): no atomics, fixed
  *     reduction order.
+ *   - Stream order: kernels may be launched with programmatic dependent launch; each waits
+ *     for the preceding work on the stream before reading the caller's input or writing
+ *     anything, so inputs produced by earlier kernels on the same stream are safe.
  */
 #ifndef NSDGT_H
 #define NSDGT_H
