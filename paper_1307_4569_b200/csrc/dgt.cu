@@ -1677,7 +1677,7 @@ static int launch_front(Plan* P, const void* f, int64_t nb, cudaStream_t st) {
         FrontArgs FA{};
         FA.f = f; FA.real_in = real_in ? 1 : 0; FA.pre = P->pre; FA.H = P->fhat;
         FA.tw = P->tw_m; FA.twL = P->twL; FA.L = I.L;
-        CUDA_TRY(launch_pdl(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes>, dim3(180 / kFrontRes, (unsigned)nb),
+        CUDA_TRY(launch_pdl(front_f4096_kernel<T, kFrontMinB, kFrontRes>, dim3(180 / kFrontRes, (unsigned)nb),
                             dim3(256 * kFrontRes), front_smem(sizeof(C)), st, FA));
         // a length-4096 DFT of 180 residues per signal (the DFT_180 runs in zak_rr0_kernel)
         prof_close(P, ph, PK_FRONTF, nb * L * ein, nb * 5.0 * L * 12.0, st);
@@ -1871,9 +1871,9 @@ static int configure(Plan* P, int64_t max_chunk) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA / 2));
         CUDA_TRY(cudaFuncSetAttribute(zak_rr_kernel<T, 8, kZrrMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zrr_smem<T>()));
         CUDA_TRY(cudaFuncSetAttribute(zak_rr0_kernel<T, 8, kZrr0MinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zrr_smem<T>()));
-        CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes>,
+        CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, kFrontMinB, kFrontRes>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem((int)e)));
-        CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes, true>,
+        CUDA_TRY(cudaFuncSetAttribute(front_f4096_kernel<T, kFrontMinB, kFrontRes, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem((int)e)));
         CUDA_TRY(cudaFuncSetAttribute(zak_rr0_adj_kernel<T, 8, kZrr0MinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       zrr_smem<T>()));
@@ -2051,7 +2051,7 @@ static int launch_inverse_tail(Plan* P, void* f, int64_t nb, cudaStream_t st) {
     if (P->front) {   // the adjoint of front_f4096 (4096-point DFTs per residue, stride-180 writes)
         FrontArgs FA{};
         FA.f = P->finv; FA.real_in = 0; FA.pre = P->pre; FA.H = f; FA.tw = P->tw_m; FA.twL = P->twL; FA.L = I.L;
-        CUDA_TRY(launch_pdl(front_f4096_kernel<T, 2 / kFrontRes, kFrontRes, true>, dim3(180 / kFrontRes, (unsigned)nb),
+        CUDA_TRY(launch_pdl(front_f4096_kernel<T, kFrontMinB, kFrontRes, true>, dim3(180 / kFrontRes, (unsigned)nb),
                             dim3(256 * kFrontRes), front_smem(sizeof(C)), st, FA));
         prof_close(P, ph, PK_FRONTF, nb * L * e, nb * 5.0 * L * 12.0, st);
         CUDA_TRY(cudaGetLastError());

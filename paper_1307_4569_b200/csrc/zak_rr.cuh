@@ -147,6 +147,10 @@ constexpr int kFrontElems = 256 * 17;   // exchange buffer per residue (elements
 #define NSDGT_FRONT_RES 2
 #endif
 constexpr int kFrontRes = NSDGT_FRONT_RES;   // residues per front_f4096 CTA
+#ifndef NSDGT_FRONT_MINB
+#define NSDGT_FRONT_MINB (2 / NSDGT_FRONT_RES)
+#endif
+constexpr int kFrontMinB = NSDGT_FRONT_MINB;   // CTAs per SM the register budget is sized for
 constexpr int front_smem(int esz) { return (kFrontRes * (kFrontElems + 4)) * esz; }
 
 // v[k] *= b0 * w^k, k < 16 (w^k from three squarings and products: <= 6 roundings)
