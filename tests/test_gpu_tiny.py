@@ -105,3 +105,20 @@ def test_input_produced_by_preceding_kernel(env, cfg):
             plan.execute(fbuf, out=out)
             got = out.clone()                    # read right after, same stream
             assert torch.equal(got, ref[k]), (rep, k)
+
+
+def test_new_paths_bitwise_deterministic(env):
+    """Shared-memory races in the round-2 kernels (one-CTA path, front_f4096, zak_rr0 and their
+    adjoints, the config-2 output loads) would show as run-to-run differences: five runs of each
+    are bit-for-bit equal (the library has no atomics and a fixed reduction order)."""
+    torch, nsdgt, oracle = env
+    for k in (0, 1, 3):
+        wl = CONFIGS[k]
+        g = window(wl)
+        f = torch.from_numpy(batch(wl, 0, min(wl.W, 3))).cuda()
+        plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, real_input=wl.real_input)
+        c0 = plan.execute(f).clone()
+        r0 = plan.inverse(c0).clone()
+        for _ in range(4):
+            assert torch.equal(plan.execute(f), c0), wl.name
+            assert torch.equal(plan.inverse(c0), r0), wl.name
