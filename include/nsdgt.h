@@ -64,7 +64,8 @@ typedef enum dgt_flags {
     DGT_G_ON_HOST = 2,       /* g is a host pointer (else a device pointer)                      */
     DGT_SHEAR_PAPER = 4,     /* choose s1 by the proof's Eq. (s1choice) and
                                 the least s0 solving Eq. (modcond), instead of the cost policy   */
-    DGT_FORCE_GENERIC = 8    /* use the generic kernels even where a specialised one exists     */
+    DGT_FORCE_GENERIC = 8    /* use the runtime-radix chunk kernels even where a specialised,
+                                fused or one-CTA kernel exists (kernel_path 0)                   */
 } dgt_flags;
 
 typedef enum dgt_branch {
@@ -86,7 +87,9 @@ typedef struct dgt_lattice_info {
     int64_t pre_sigma;                   /* sigma of the pre-FFT chirp (F-branch, 0 = none)         */
     int64_t chunk;                       /* signals per on-chip/L2 chunk (dgt_plan only)            */
     int64_t workspace_bytes;             /* device workspace owned by the plan (dgt_plan only)      */
-    int64_t kernel_path;                 /* 0 generic, >0 specialised kernel id (dgt_plan only)     */
+    int64_t kernel_path;                 /* 0 chunk kernels, 2 fused persistent kernel, 4 the
+                                            frequency-shear front path (L = 180 x 4096), 8 the
+                                            one-CTA path for short signals (dgt_plan)          */
 } dgt_lattice_info;
 
 typedef struct dgt_plan_s* dgt_plan_t;

@@ -1820,7 +1820,10 @@ static int configure(Plan* P, int64_t max_chunk) {
     // compile-time Zak kernels (p = 1, q = 4, all-u mode): d = 180 with RB = 64 / e columns
     // (config 4), d = 720 with one column per CTA (config 2)
     P->zct = 0;
-    if (P->allu && I.q == 4 && I.c % P->RB == 0 && !std::getenv("NSDGT_ZAK_RT")) {
+    // DGT_FORCE_GENERIC: the runtime-radix chunk kernels only (no compile-time, register-resident,
+    // one-CTA or fused kernel)
+    const bool forced = (P->flags & DGT_FORCE_GENERIC) != 0;
+    if (P->allu && I.q == 4 && I.c % P->RB == 0 && !std::getenv("NSDGT_ZAK_RT") && !forced) {
         if (I.d == 180 && P->RB == (int)(64 / e)) P->zct = 180;
         if (I.d == 720 && P->RB == 1) P->zct = 720;
         // c128 forward: 128-thread CTAs of RB / 2 columns (32-byte rows), 4 CTAs per SM -- finer
@@ -1880,11 +1883,11 @@ static int configure(Plan* P, int64_t max_chunk) {
     }
     CUDA_TRY(cudaFuncSetAttribute(out_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
     // compile-time output DFT for M' = 200 (config 2, time shear)
-    P->outct = (I.branch != DGT_BRANCH_FREQ && I.iM == 200 && !P->gB && !std::getenv("NSDGT_OUT_GENERIC")) ? 200 : 0;
+    P->outct = (I.branch != DGT_BRANCH_FREQ && I.iM == 200 && !P->gB && !std::getenv("NSDGT_OUT_GENERIC") && !forced) ? 200 : 0;
     if (P->outct) CUDA_TRY(cudaFuncSetAttribute(out_kernel<T, 200>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
     // out_f4096: 2 CTAs per SM for c128 (128 registers, measured faster than 3 CTAs at 80
     // registers with spills), 3 for c64
-    P->outk = (I.branch == DGT_BRANCH_FREQ && I.iM == 4096 && !std::getenv("NSDGT_OUT_GENERIC")) ? (e == 16 ? 2 : 1) : 0;
+    P->outk = (I.branch == DGT_BRANCH_FREQ && I.iM == 4096 && !std::getenv("NSDGT_OUT_GENERIC") && !forced) ? (e == 16 ? 2 : 1) : 0;
     if (P->outk && std::getenv("NSDGT_OUTF_MINB")) P->outk = std::atoi(std::getenv("NSDGT_OUTF_MINB")) == 2 ? 2 : 1;   // experiment
     // zak_ct (d = 180) feeding out_f4096: the intermediate is stored [n][j] so the output
     // kernel's column loads are contiguous (NSDGT_CNJ_OFF: the generic [j][kappa][n'] layout)
@@ -1899,7 +1902,7 @@ static int configure(Plan* P, int64_t max_chunk) {
         const bool freq = I.branch == DGT_BRANCH_FREQ;
         const int64_t te = tiny_elems(I.L, I.q, I.p, I.d, I.iM, freq);
         const Radices rl = make_radices((int)std::min<int64_t>(I.L, 1 << 30));
-        P->tiny = (!std::getenv("NSDGT_TINY_OFF") && te * (int64_t)e <= 160 * 1024 && I.iM * I.iN == I.L / I.p * I.q &&
+        P->tiny = (!std::getenv("NSDGT_TINY_OFF") && !forced && te * (int64_t)e <= 160 * 1024 && I.iM * I.iN == I.L / I.p * I.q &&
                    I.iM == I.c * I.q && rl.nst <= kMaxStages) ? 1 : 0;
         if (P->tiny) {
             P->rd_L = rl;
@@ -2324,7 +2327,8 @@ static int make_plan(dgt_plan_t* out, int64_t L, int64_t a, int64_t M, int64_t l
     }
     P->info.chunk = P->chunk;
     P->info.workspace_bytes = (int64_t)P->ws_bytes;
-    P->info.kernel_path = P->fast;
+    // 2 fused persistent kernel, 4 config-4 front path (front_f4096 + zak_rr0), 8 one-CTA path
+    P->info.kernel_path = P->fast ? P->fast : (P->tiny ? 8 : (P->front ? 4 : 0));
     *out = (dgt_plan_t)P;
     return DGT_OK;
 }

@@ -324,14 +324,18 @@ def test_linearity_and_determinism(torch_cuda, nsdgt):
 
 
 def test_fast_path_matches_generic(torch_cuda, nsdgt):
-    """Where a specialised kernel exists it agrees with the generic kernels."""
+    """Where a specialised kernel exists it agrees with the generic kernels (DGT_FORCE_GENERIC:
+    the runtime-radix chunk kernels only): the fused kernel (configs 3, 5, kernel_path 2), the
+    compile-time config-2 kernels, the config-4 front path (4) and the one-CTA path (config 1, 8)."""
     torch = torch_cuda
-    for k in (3, 5, 2, 4):
+    for k, path in ((3, 2), (5, 2), (2, 0), (4, 4), (1, 8)):
         wl = CONFIGS[k - 1]
         g = window(wl)
-        f = batch(wl, 0, 2)
-        pf = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype)
-        pg = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, force_generic=True)
+        f = batch(wl, 0, min(wl.W, 2))
+        pf = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, real_input=wl.real_input)
+        assert pf.info["kernel_path"] == path, (k, pf.info["kernel_path"])
+        pg = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype=wl.dtype, real_input=wl.real_input,
+                        force_generic=True)
         assert pg.info["kernel_path"] == 0
         ft = torch.from_numpy(f).cuda()
         a_ = pf.execute(ft).cpu().numpy()
