@@ -27,6 +27,7 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include "../../include/nsdgt.h"
@@ -223,6 +224,27 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// The same with a thread-block cluster of cx CTAs along x.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                      unsigned cx, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = cx;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -633,6 +655,22 @@ __device__ __forceinline__ void fb_column(const OutArgs& A, C* out, unsigned lon
     }
 }
 
+// fb_column's iteration, handing each coefficient's destination and phase to put(i, dst, ph)
+template <int CNT, typename C, class Put>
+__device__ __forceinline__ void fb_column_dest(const OutArgs& A, unsigned long long m, unsigned int kc0, Put&& put) {
+    const FbCol cc = fb_col(A, m);
+    FbIter<C> it = fb_iter<C>(A, cc, kc0 ? (unsigned long long)A.Nr - kc0 : 0ull);
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+        if (i == 1 && kc0 == 0) it = fb_iter<C>(A, cc, (unsigned long long)A.Nr - 256u);
+        else if (i > 0) fb_step(A, it);
+        size_t dst;
+        C ph;
+        fb_dest(A, it, &dst, &ph);
+        put(i, dst, ph);
+    }
+}
+
 // IMCT > 0: compile-time inner channel count (its DFT by fft_ct; config 2: 200)
 template <typename T, int IMCT = 0>
 __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
@@ -770,7 +808,13 @@ __device__ __forceinline__ void twiddle15(C* v, const C* __restrict__ tw, int s)
     v[15] = cmul(v[15], cmul(w7, w8));
 }
 
-template <typename T, int MINB>
+// CL (config 4, clusters of 3 CTAs): the three inner columns m = 3 kt + i fill output row kt,
+// column i the positions mt = i (mod 3) (checked at plan time, k_cl_check).  Each CTA stages
+// E(k, m) X(kc) at slot mt / 3 of its shared memory; after a cluster barrier CTA i copies row
+// positions [4096 i, 4096 i + 4096) out of the three CTAs' shared memory (distributed shared
+// memory) with contiguous 16-byte stores -- instead of each column's 16-byte stores at a
+// 48-byte stride.
+template <typename T, int MINB, bool CL = false>
 __global__ void __launch_bounds__(256, MINB) out_f4096_kernel(OutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
@@ -806,9 +850,47 @@ __global__ void __launch_bounds__(256, MINB) out_f4096_kernel(OutArgs A) {
     for (int t1 = 0; t1 < 16; ++t1) v[t1] = S[hi * 272 + 17 * lo + t1];
     dft16<T>(v);
     C* out = (C*)A.out + w * A.M * A.N;
-    fb_column<16>(A, out, (unsigned long long)m, (unsigned int)(hi + 16 * lo), 16, [&](int i) { return v[i]; });
+    if constexpr (CL) {
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        const int kt = m / 3;
+        const size_t rowb = (size_t)kt * (size_t)A.N;
+        __syncthreads();   // every pass-3 read of S is done
+        fb_column_dest<16, C>(A, (unsigned long long)m, (unsigned int)(hi + 16 * lo),
+                              [&](int i, size_t dst, C ph) { S[(dst - rowb) / 3] = cmul(ph, v[i]); });
+        cl.sync();
+        const int r = (int)cl.block_rank();
+        C y[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int mt = 4096 * r + tid + 256 * j;
+            const C* rs = cl.map_shared_rank(S, mt % 3);
+            y[j] = rs[mt / 3];
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[rowb + 4096 * r + tid + 256 * j] = y[j];
+        cl.sync();   // no CTA leaves while another reads its shared memory
+    } else {
+        fb_column<16>(A, out, (unsigned long long)m, (unsigned int)(hi + 16 * lo), 16, [&](int i) { return v[i]; });
+    }
 }
 constexpr size_t kOutF4096Elems = 16 * 272;
+
+// Plan time: does config 4's cluster variant apply -- for every inner column m and channel
+// kc, the destination row is m / 3 and the position is m (mod 3), within 3 x 4096?
+template <typename T>
+__global__ void k_cl_check(OutArgs A, int* bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.iN * A.iM) return;
+    const int m = (int)(i / A.iM), kc = (int)(i % A.iM);
+    const FbCol cc = fb_col(A, (unsigned long long)m);
+    const FbIter<cx<T>> it = fb_iter<cx<T>>(A, cc, kc ? (unsigned long long)A.Nr - kc : 0ull);
+    size_t dst;
+    cx<T> ph;
+    fb_dest(A, it, &dst, &ph);
+    const size_t row = dst / (size_t)A.N, mt = dst % (size_t)A.N;
+    if (row != (size_t)(m / 3) || mt % 3 != (size_t)(m % 3) || mt >= 3 * 4096) atomicExch(bad, 1);
+}
 
 #include "tiny.cuh"
 
@@ -1397,6 +1479,7 @@ struct Plan {
     int outct = 0;           // out_kernel compile-time inner channel count (0 = runtime radices)
     int zrr = 0;             // forward Zak with zak_rr_kernel (d = 180 = 12 x 15 in registers)
     int front = 0;           // F-branch front end by front_f4096_kernel + zak_rr0_kernel (L = 180 x 4096)
+    int outcl = 0;           // config 4: out_f4096 in clusters of 3 CTAs staging whole rows (k_cl_check)
     int tiny = 0;            // whole transform of a signal in one CTA (tiny.cuh)
     unsigned int* tiny_dst = nullptr;   // F-branch output remap table (tiny.cuh)
     void* tiny_ph = nullptr;
@@ -1597,6 +1680,25 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
         CUDA_TRY(cudaMalloc(&P->ptab, sizeof(C) * 2 * I.N));
         k_phase_table<T><<<grid_for(2 * I.N), 256, 0, st>>>((C*)P->ptab, I.N);
     }
+    // experiment (NSDGT_OUTCL=1): out_f4096 in clusters of 3 CTAs staging whole output rows in
+    // distributed shared memory -- parity-tested, measured slower (0.64 against 0.44 ms per 16
+    // signals: two cluster barriers and 64 KB of DSMEM reads per CTA), off by default
+    if (P->outk == 2 && P->cnj && I.iN % 3 == 0 && I.N == 3 * 4096 && I.iM == 4096 && std::getenv("NSDGT_OUTCL")) {
+        int* bad = nullptr;
+        CUDA_TRY(cudaMalloc(&bad, sizeof(int)));
+        CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
+        const OutArgs B = make_out_args(P, nullptr, nullptr);
+        const int64_t n = I.iN * I.iM;
+        k_cl_check<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B, bad);
+        int hb = 1;
+        CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        cudaFree(bad);
+        P->outcl = hb == 0 ? 1 : 0;
+        if (P->outcl)
+            CUDA_TRY(cudaFuncSetAttribute(out_f4096_kernel<T, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(kOutF4096Elems * sizeof(C))));
+    }
     if (P->tiny && I.branch == DGT_BRANCH_FREQ) {   // the one-CTA path's output remap table
         const int64_t n = I.iM * I.iN;
         CUDA_TRY(cudaMalloc(&P->tiny_dst, sizeof(unsigned int) * n));
@@ -1758,6 +1860,9 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     if (P->outk == 1)
         le = launch_pdl(out_f4096_kernel<T, 3>, dim3((unsigned)I.iN, (unsigned)Wc), dim3(256), kOutF4096Elems * sizeof(C),
                         st, B);
+    else if (P->outk == 2 && P->outcl)
+        le = launch_pdl_cluster(out_f4096_kernel<T, 2, true>, dim3((unsigned)I.iN, (unsigned)Wc), dim3(256),
+                                kOutF4096Elems * sizeof(C), st, 3u, B);
     else if (P->outk == 2)
         le = launch_pdl(out_f4096_kernel<T, 2>, dim3((unsigned)I.iN, (unsigned)Wc), dim3(256), kOutF4096Elems * sizeof(C),
                         st, B);

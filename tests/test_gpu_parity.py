@@ -579,3 +579,17 @@ def test_full_size_covariances(torch_cuda, nsdgt):
     wn = ((n * wl.lam1) % wl.lam2) / wl.lam2
     ph = np.exp(-2j * np.pi * x * (m + wn) / wl.M)
     assert rel(c[2], ph * np.roll(c[0], wl.lam2 * j, axis=1)) <= 5e-5
+
+
+def test_config4_cluster_output_variant(torch_cuda, nsdgt, monkeypatch):
+    """The experiment variant of config 4's output kernel (NSDGT_OUTCL=1: clusters of 3 CTAs
+    staging each output row in distributed shared memory, then contiguous stores) writes the
+    same coefficients bit for bit (same arithmetic, other store order)."""
+    torch = torch_cuda
+    wl = CONFIGS[3]
+    g = window(wl)
+    f = torch.from_numpy(batch(wl, 0, 2)).cuda()
+    c0 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c128").execute(f)
+    monkeypatch.setenv("NSDGT_OUTCL", "1")
+    c1 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c128").execute(f)
+    assert torch.equal(c0, c1)
