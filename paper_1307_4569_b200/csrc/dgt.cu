@@ -1876,6 +1876,34 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     return DGT_OK;
 }
 
+// The constant-memory twiddles W_180, W_720 of fft_ct / dft_pq (same values for every plan;
+// long-double cos/sin of exact residues on the host, rounded once).  __constant__ memory is per
+// device: uploaded once per device (a mutex-guarded set of devices; a failed upload is retried
+// by the next plan instead of poisoning it).  Used by the compile-time Zak kernels, zak_rr* and
+// the one-CTA path's compile-time variant.
+static bool upload_const_twiddles() {
+    static std::mutex tw_mu;
+    static std::set<int> tw_done;
+    std::lock_guard<std::mutex> lk(tw_mu);
+    auto fill = [](auto& dsym, auto& fsym, int n) {
+        std::vector<double2> d(n);
+        std::vector<float2> f(n);
+        for (int k = 0; k < n; ++k) {
+            const long double th = -2.0L * 3.141592653589793238462643383279502884L * (long double)k / (long double)n;
+            d[k] = make_double2((double)cosl(th), (double)sinl(th));
+            f[k] = make_float2((float)d[k].x, (float)d[k].y);
+        }
+        return cudaMemcpyToSymbol(dsym, d.data(), sizeof(double2) * n) == cudaSuccess &&
+               cudaMemcpyToSymbol(fsym, f.data(), sizeof(float2) * n) == cudaSuccess;
+    };
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (tw_done.count(dev)) return true;
+    if (!fill(c_tw180d, c_tw180f, 180) || !fill(c_tw720d, c_tw720f, 720)) return false;
+    tw_done.insert(dev);
+    return true;
+}
+
 template <typename T>
 static int configure(Plan* P, int64_t max_chunk) {
     const dgt_lattice_info& I = P->info;
@@ -1945,34 +1973,7 @@ static int configure(Plan* P, int64_t max_chunk) {
                     !std::getenv("NSDGT_FRONT_CUFFT")) ? 1 : 0;
     }
     if (P->zct) {
-        // the constant-memory twiddles of fft_ct (same values for every plan; long-double
-        // cos/sin of exact residues on the host, rounded once)
-        // __constant__ memory is per device: upload once per device (mutex-guarded set of
-        // devices done; a failed upload is retried by the next plan instead of poisoning it)
-        static std::mutex tw_mu;
-        static std::set<int> tw_done;
-        int tw_rc = 0;
-        {
-            std::lock_guard<std::mutex> lk(tw_mu);
-            auto fill = [](auto& dsym, auto& fsym, int n) {
-                std::vector<double2> d(n);
-                std::vector<float2> f(n);
-                for (int k = 0; k < n; ++k) {
-                    const long double th = -2.0L * 3.141592653589793238462643383279502884L * (long double)k / (long double)n;
-                    d[k] = make_double2((double)cosl(th), (double)sinl(th));
-                    f[k] = make_float2((float)d[k].x, (float)d[k].y);
-                }
-                return cudaMemcpyToSymbol(dsym, d.data(), sizeof(double2) * n) == cudaSuccess &&
-                       cudaMemcpyToSymbol(fsym, f.data(), sizeof(float2) * n) == cudaSuccess;
-            };
-            int dev = -1;
-            cudaGetDevice(&dev);
-            if (!tw_done.count(dev)) {
-                if (!fill(c_tw180d, c_tw180f, 180) || !fill(c_tw720d, c_tw720f, 720)) tw_rc = 1;
-                else tw_done.insert(dev);
-            }
-        }
-        if (tw_rc) return fail(DGT_ECUDA, "constant twiddle upload");
+        if (!upload_const_twiddles()) return fail(DGT_ECUDA, "constant twiddle upload");
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_kernel<T, 720, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
@@ -2013,6 +2014,13 @@ static int configure(Plan* P, int64_t max_chunk) {
             P->rd_L = rl;
             P->tiny_smem = (size_t)te * e;
             CUDA_TRY(cudaFuncSetAttribute(tiny_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->tiny_smem));
+            // config 1's shape as a compile-time variant (NSDGT_TINY_RT keeps the runtime one)
+            if (I.L == 240 && I.c == 5 && I.d == 8 && I.p == 2 && I.q == 3 && freq && !std::getenv("NSDGT_TINY_RT")) {
+                if (!upload_const_twiddles()) return fail(DGT_ECUDA, "constant twiddle upload");   // dft_pq's W_15
+                P->tiny = 2;
+                CUDA_TRY(cudaFuncSetAttribute(tiny_kernel<T, 240, 5, 8, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)P->tiny_smem));
+            }
         }
     }
     P->inv_generic = std::getenv("NSDGT_INV_GENERIC") ? 1 : 0;
@@ -2305,7 +2313,10 @@ static int launch_tiny(Plan* P, const void* f, void* c, int64_t W, cudaStream_t 
         TinyArgs Tw = TA;
         Tw.f = (const char*)f + (size_t)w0 * I.L * (size_t)ein;
         Tw.B.out = (char*)c + (size_t)w0 * I.M * I.N * P->esz;
-        CUDA_TRY(launch_pdl(tiny_kernel<T>, dim3((unsigned)wc), dim3(256), P->tiny_smem, st, Tw));
+        if (P->tiny == 2)
+            CUDA_TRY(launch_pdl(tiny_kernel<T, 240, 5, 8, 2, 3>, dim3((unsigned)wc), dim3(256), P->tiny_smem, st, Tw));
+        else
+            CUDA_TRY(launch_pdl(tiny_kernel<T>, dim3((unsigned)wc), dim3(256), P->tiny_smem, st, Tw));
     }
     prof_close(P, ph, PK_TINY, W * (L * ein + MN * e) + L * e, fl, st);
     CUDA_TRY(cudaGetLastError());

@@ -73,11 +73,50 @@ __device__ unsigned long long g_tiny_trace[16];
 #define TINY_MARK(k) do { } while (0)
 #endif
 
-template <typename T>
+// One Stockham pass of compile-time radix R on nseq sequences of compile-time length N (the
+// one-CTA path's compile-time variant): R = 15 runs as 3 x 5 in registers (inner twiddles
+// W_15 = W_180^12 from the constant table), other radices as register butterflies.
+template <typename T, int N, int R, int NS>
+__device__ __forceinline__ void tstage(const cx<T>* __restrict__ in, cx<T>* __restrict__ out, int nseq,
+                                       const cx<T>* __restrict__ tw) {
+    using C = cx<T>;
+    constexpr int nb = N / R, tstep = N / (NS * R);
+    for (int t = threadIdx.x; t < nb * nseq; t += blockDim.x) {
+        const int seq = t / nb, j = t - seq * nb;
+        const int k = j % NS;
+        const C* src = in + seq * N;
+        C* dst = out + seq * N;
+        C v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = src[j + r * nb];
+        if constexpr (NS > 1) {
+            const C w1 = tw[k * tstep];
+            C wr = w1;
+            v[1] = cmul(v[1], w1);
+#pragma unroll
+            for (int r = 2; r < R; ++r) {
+                wr = cmul(wr, w1);
+                v[r] = cmul(v[r], wr);
+            }
+        }
+        if constexpr (R == 15) dft_pq<T, 3, 5, 180>(v, 12);
+        else dft_fixed<T, R>(v);
+        const int base = (j / NS) * NS * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[base + r * NS] = v[r];
+    }
+}
+
+// SL > 0: a compile-time lattice shape (L, c, d, p, q) = (SL, SC, SD, SP, SQ) -- config 1's
+// (240, 5, 8, 2, 3): every index divides by constants and the DFTs run as compile-time passes
+// (DFT_240 = 16 x 15, DFT_8, DFT_15 = 3 x 5 in one pass) instead of the runtime-radix engine.
+template <typename T, int SL = 0, int SC = 0, int SD = 0, int SP = 0, int SQ = 0>
 __global__ void __launch_bounds__(256) tiny_kernel(const __grid_constant__ TinyArgs A) {
     using C = cx<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int L = A.L, c = A.c, d = A.d, p = A.p, q = A.q, iM = A.iM, iN = A.iN;
+    constexpr bool CT = SL > 0;
+    const int L = CT ? SL : A.L, c = CT ? SC : A.c, d = CT ? SD : A.d, p = CT ? SP : A.p, q = CT ? SQ : A.q;
+    const int iM = CT ? SC * SQ : A.iM, iN = CT ? SQ * SD : A.iN;
     const bool freq = A.B.branch == DGT_BRANCH_FREQ;
     const int LQ = L / p * q;
     const int LX = LQ > L ? LQ : L;
@@ -134,7 +173,18 @@ __global__ void __launch_bounds__(256) tiny_kernel(const __grid_constant__ TinyA
     __syncthreads();
     TINY_MARK(1);
     // ---- 1. F-branch: f^ = DFT_L(f) ----
-    const C* fh = freq ? fft_smem<T>(sF, sF2, A.rdL, 1, L, sTwL) : sF;
+    const C* fh = sF;
+    if constexpr (CT) {
+        static_assert(SL == 240 && SD == 8 && SC * SQ == 15, "compile-time shape: config 1 only");
+        if (freq) {
+            tstage<T, 240, 16, 1>(sF, sF2, 1, sTwL);
+            __syncthreads();
+            tstage<T, 240, 15, 16>(sF2, sF, 1, sTwL);
+            __syncthreads();
+        }
+    } else if (freq) {
+        fh = fft_smem<T>(sF, sF2, A.rdL, 1, L, sTwL);
+    }
     TINY_MARK(2);
     // ---- 2. Zak gather of all (l, r, k, s): sX[((l c + r) p + k) d + s] ----
     {
@@ -151,7 +201,14 @@ __global__ void __launch_bounds__(256) tiny_kernel(const __grid_constant__ TinyA
     __syncthreads();
     TINY_MARK(3);
     // ---- 3. DFT_d over s ----
-    C* phi = fft_smem<T>(sX, sY, A.rdd, q * c * p, d, sTwd);
+    C* phi;
+    if constexpr (CT) {
+        tstage<T, 8, 8, 1>(sX, sY, q * c * p, sTwd);
+        __syncthreads();
+        phi = sY;
+    } else {
+        phi = fft_smem<T>(sX, sY, A.rdd, q * c * p, d, sTwd);
+    }
     TINY_MARK(4);
     C* Yb = phi == sX ? sY : sX;
     // ---- 4. products Y(l, r, u; nu) at Yb[((l c + r) q + u) d + nu] ----
@@ -168,7 +225,14 @@ __global__ void __launch_bounds__(256) tiny_kernel(const __grid_constant__ TinyA
     __syncthreads();
     TINY_MARK(5);
     // ---- 5. DFT_d over nu; scatter to C[n][j] ----
-    C* Yd = fft_smem<T>(Yb, phi, A.rdd, q * c * q, d, sTwd);   // phi is dead: its buffer is scratch
+    C* Yd;   // phi is dead: its buffer is the scratch
+    if constexpr (CT) {
+        tstage<T, 8, 8, 1>(Yb, phi, q * c * q, sTwd);
+        __syncthreads();
+        Yd = phi;
+    } else {
+        Yd = fft_smem<T>(Yb, phi, A.rdd, q * c * q, d, sTwd);
+    }
     TINY_MARK(6);
     C* Cn = Yd == sX ? sY : sX;
     for (int i = tid; i < LQ; i += nt) {
@@ -186,7 +250,14 @@ __global__ void __launch_bounds__(256) tiny_kernel(const __grid_constant__ TinyA
     __syncthreads();
     TINY_MARK(7);
     // ---- 6. DFT over j of the iN columns ----
-    C* X = fft_smem<T>(Cn, Yd, A.rdm, iN, iM, sTwm);
+    C* X;
+    if constexpr (CT) {
+        tstage<T, 15, 15, 1>(Cn, Yd, iN, sTwm);
+        __syncthreads();
+        X = Yd;
+    } else {
+        X = fft_smem<T>(Cn, Yd, A.rdm, iN, iM, sTwm);
+    }
     TINY_MARK(8);
     // ---- 7. output ----
     C* out = (C*)A.B.out + w * A.B.M * A.B.N;
