@@ -205,6 +205,21 @@ __global__ void k_prechirp(cx<T>* out, const void* f, int real_in, const cx<T>* 
     }
 }
 
+#ifdef NSDGT_KTRACE
+// experiment builds only (tools/ktrace.py): %globaltimer at phase boundaries of block (0, 0)
+__device__ unsigned long long g_ktrace[64];
+#define KTRACE(k)                                                                               \
+    do {                                                                                        \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {                           \
+            unsigned long long t_;                                                              \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+            g_ktrace[k] = t_;                                                                   \
+        }                                                                                       \
+    } while (0)
+#else
+#define KTRACE(k) do { } while (0)
+#endif
+
 // Launch with the programmatic-serialisation attribute (PDL; cplx.cuh pdl_wait / pdl_trigger):
 // the kernel's launch and prologue overlap its predecessor's tail.  NSDGT_PDL_OFF: plain launch.
 static bool pdl_enabled() {
@@ -404,10 +419,14 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
     const int rblk = blockIdx.x % nrb, l = blockIdx.x / nrb;
     const int64_t w = blockIdx.y;
     const int r0 = rblk * RBC;
-    // d = 720 (one column per CTA, config 2): the window factors are loaded first, their
-    // latency under the gather and the first DFT (a plan table: before the PDL wait)
-    constexpr bool EG = D == 720;
+    // d = 720 (one column per CTA, config 2), experiment builds: the window factors loaded
+    // first (a plan table: before the PDL wait) -- slower, the gather's loads queue behind them
+#ifndef NSDGT_ZCT_EG   // window factors before the gather: measured slower (33.0 vs 31.8 us, config 2)
+#define NSDGT_ZCT_EG 0
+#endif
+    constexpr bool EG = D == 720 && NSDGT_ZCT_EG;
     C gv[NP];
+    KTRACE(0);
     pdl_trigger();
     if constexpr (EG) {
         const C* __restrict__ G = (const C*)A.G;
@@ -457,7 +476,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
         }
     }
     __syncthreads();
+    KTRACE(1);
     C* phi = fft_ct<T, D>(R1, R2, RBC, tw);     // Phi in the first RBC D of R1 or R2
+    KTRACE(2);
     C* Yb = phi == R1 ? R2 : R1;
     {
         const C* __restrict__ G = (const C*)A.G;
@@ -478,7 +499,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
         }
     }
     __syncthreads();
+    KTRACE(3);
     C* Y = fft_ct<T, D>(Yb, phi, Q * RBC, tw);   // Phi is dead: its buffer is the scratch
+    KTRACE(4);
     C* Cw = (C*)A.C + w * A.iM * Q * D;
     const int jbase = r0 + c * (l % Q);
     if (A.cnj) {
@@ -510,6 +533,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
             Cw[((jbase + rr) * Q + kappa) * D + np] = Y[(u * RBC + rr) * D + tau];
         }
     }
+#ifdef NSDGT_KTRACE
+    __syncthreads();
+#endif
+    KTRACE(5);
 }
 
 #include "zak_rr.cuh"
@@ -700,6 +727,7 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
     // T-branch with blockDim = 256 and nt | 256 (this tile's column count): thread t's output
     // column is always nb + t mod nt, so its E(n) and rot(n) (plan tables) are loaded once,
     // before the PDL wait
+    KTRACE(10);
     C Et = mk<T>(T(1), T(0));
     int rott = 0;
     const bool colfix = A.branch != DGT_BRANCH_FREQ && nt > 0 && 256 % nt == 0;
@@ -758,9 +786,11 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
         }
     }
     __syncthreads();
+    KTRACE(11);
     C* X;
     if constexpr (IMCT > 0) X = fft_ct<T, IMCT>(bufA, bufB, nt, (const C*)A.tw);
     else X = fft_smem<T>(bufA, bufB, A.rd, nt, (int)iM, (const C*)A.tw);
+    KTRACE(12);
     if (A.branch != DGT_BRANCH_FREQ) {
         // c[w][(m - rot(n)) mod M][n] = E(n) * X(m, n)   (Alg. 1 lines 9-12)
         C* out = (C*)A.out + w * A.M * A.N;
@@ -774,6 +804,10 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
             if (m >= Mi) m -= Mi;
             out[mo * Ni + n] = cmul(colfix ? Et : E[n], X[cl * iMi + m]);
         }
+#ifdef NSDGT_KTRACE
+        __syncthreads();
+#endif
+        KTRACE(13);
     } else {
         C* out = (C*)A.out + w * A.M * A.N;
         for (int cl = 0; cl < nt; ++cl) {
@@ -2869,6 +2903,11 @@ void* dgt_debug_trace_log(dgt_plan_t plan) {
     return P ? (void*)P->fp.tracelog : nullptr;
 }
 
+#ifdef NSDGT_KTRACE
+int dgt_debug_ktrace(unsigned long long* out64) {   // experiment builds only
+    return cudaMemcpyFromSymbol(out64, g_ktrace, sizeof(unsigned long long) * 64) == cudaSuccess ? 0 : 1;
+}
+#endif
 #ifdef NSDGT_TINY_TRACE
 int dgt_debug_tiny_trace(unsigned long long* out16) {   // experiment builds only
     return cudaMemcpyFromSymbol(out16, g_tiny_trace, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : 1;
