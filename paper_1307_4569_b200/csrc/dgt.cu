@@ -1546,10 +1546,10 @@ struct Plan {
 };
 
 enum ProfKind { PK_FRONT = 0, PK_ZAK = 1, PK_OUT = 2, PK_FAST = 3, PK_ZAKCT = 4, PK_OUTF = 5, PK_ZAKADJ = 6,
-                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_FRONTF = 10, PK_ZAKRR = 11, PK_TINY = 12, PK_COUNT = 13 };
+                PK_OUTADJ = 7, PK_FASTADJ = 8, PK_MW = 9, PK_FRONTF = 10, PK_ZAKRR = 11, PK_TINY = 12, PK_TINYADJ = 13, PK_COUNT = 14 };
 static const char* kProfNames[PK_COUNT] = {"front_fft_cufft", "zak_generic", "out_generic", "fused_fast",
                                            "zak_ct", "out_f4096", "zak_adjoint", "out_adjoint",
-                                           "fused7a_t_p1", "multiwindow_interleave", "front_f4096", "zak_rr", "tiny"};
+                                           "fused7a_t_p1", "multiwindow_interleave", "front_f4096", "zak_rr", "tiny", "tiny_adjoint"};
 
 static cudaEvent_t prof_event(Plan* P) {
     if (P->pool_used == P->pool.size()) {
@@ -2048,12 +2048,15 @@ static int configure(Plan* P, int64_t max_chunk) {
             P->rd_L = rl;
             P->tiny_smem = (size_t)te * e;
             CUDA_TRY(cudaFuncSetAttribute(tiny_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->tiny_smem));
+            CUDA_TRY(cudaFuncSetAttribute(tiny_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->tiny_smem));
             // config 1's shape as a compile-time variant (NSDGT_TINY_RT keeps the runtime one)
             if (I.L == 240 && I.c == 5 && I.d == 8 && I.p == 2 && I.q == 3 && freq && !std::getenv("NSDGT_TINY_RT")) {
                 if (!upload_const_twiddles()) return fail(DGT_ECUDA, "constant twiddle upload");   // dft_pq's W_15
                 P->tiny = 2;
                 CUDA_TRY(cudaFuncSetAttribute(tiny_kernel<T, 240, 5, 8, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)P->tiny_smem));
+                CUDA_TRY(cudaFuncSetAttribute(tiny_adj_kernel<T, 240, 5, 8, 2, 3>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->tiny_smem));
             }
         }
     }
@@ -2217,8 +2220,40 @@ static int launch_inverse_tail(Plan* P, void* f, int64_t nb, cudaStream_t st) {
     return DGT_OK;
 }
 
+// Synthesis on the one-CTA path (tiny.cuh, tiny_adj_kernel): one CTA per signal.
+template <typename T>
+static int launch_tiny_adj(Plan* P, const void* c, void* f, int64_t W, cudaStream_t st) {
+    const dgt_lattice_info& I = P->info;
+    TinyArgs TA = P->tiny_args;
+    TA.f = nullptr; TA.real_in = 0;
+    TA.rdL = P->rd_L; TA.rdd = P->rd_d; TA.rdm = P->rd_m;
+    TA.L = (int)I.L; TA.c = (int)I.c; TA.d = (int)I.d; TA.p = (int)I.p; TA.q = (int)I.q;
+    TA.iM = (int)I.iM; TA.iN = (int)I.iN;
+    TA.B = make_out_args(P, nullptr, nullptr);
+    const double e = (double)P->esz, L = (double)I.L, MN = (double)I.M * (double)I.N;
+    const double fl = W * ((I.branch == DGT_BRANCH_FREQ ? 4.0 * L * std::log2(L) : 0.0) + 8.0 * L * I.q / I.p +
+                           4.0 * L * std::log2((double)I.d) + 4.0 * MN * std::log2((double)I.d) +
+                           4.0 * MN * std::log2((double)I.iM) + 6.0 * MN);
+    const int ph = prof_open(P, st);
+    for (int64_t w0 = 0; w0 < W; w0 += 65535 * 1024) {
+        const int64_t wc = std::min<int64_t>(65535 * 1024, W - w0);
+        const void* cc = (const char*)c + (size_t)w0 * I.M * I.N * P->esz;
+        void* fc = (char*)f + (size_t)w0 * I.L * P->esz;
+        if (P->tiny == 2)
+            CUDA_TRY(launch_pdl(tiny_adj_kernel<T, 240, 5, 8, 2, 3>, dim3((unsigned)wc), dim3(256), P->tiny_smem, st, TA,
+                                cc, fc));
+        else
+            CUDA_TRY(launch_pdl(tiny_adj_kernel<T>, dim3((unsigned)wc), dim3(256), P->tiny_smem, st, TA, cc, fc));
+    }
+    prof_close(P, ph, PK_TINYADJ, W * (L + MN) * e + L * e, fl, st);
+    CUDA_TRY(cudaGetLastError());
+    return DGT_OK;
+}
+
 static int execute_inverse(Plan* P, const void* c, void* f, int64_t W, cudaStream_t st) {
     const dgt_lattice_info& I = P->info;
+    if (P->tiny && !P->fast)
+        return P->dtype == DGT_C64 ? launch_tiny_adj<float>(P, c, f, W, st) : launch_tiny_adj<double>(P, c, f, W, st);
     if (P->fast && !P->inv_generic) {
         // fused synthesis (fused7_adj.cuh) on the forward ring
         const int ph = prof_open(P, st);

@@ -284,3 +284,161 @@ __global__ void __launch_bounds__(256) tiny_kernel(const __grid_constant__ TinyA
     __syncthreads();
     TINY_MARK(9);
 }
+
+// Synthesis on the one-CTA path (dgt_execute_inverse of short signals): the adjoint of
+// tiny_kernel, step by step in reverse, every value kept conjugated so that each DFT is a
+// forward one (conj(DFT^H(y)) = DFT(conj y)); the conjugations fold into the first loads and
+// the last stores.  Steps (z = conj of the adjoint's value):
+//   7'. z(n, kc) = ph conj(c[dst]) (F-branch remap table) / E(n) conj(c[(m - rot n) mod M][n])
+//   6'. DFT over kc of each column n                       -> z = conj C'(n, j)
+//   5'. gather through the forward scatter map into rows (l, r, u), DFT_d over tau
+//   4'. acc(l, r, k; nu) = sum_u z(l, r, u; nu) G(r, u, k; nu)
+//   3'. DFT_d over nu                                       -> z = conj v'(l, r, k; s)
+//   2'. scatter through the Zak map with the chirp: z(x) = chirp(x) z(l, r, k; s)
+//   1'. F-branch: DFT_L, f = conj(pre z); T-branch: f = conj(z)
+template <typename T, int SL = 0, int SC = 0, int SD = 0, int SP = 0, int SQ = 0>
+__global__ void __launch_bounds__(256) tiny_adj_kernel(const __grid_constant__ TinyArgs A, const void* cin, void* fout) {
+    using C = cx<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr bool CT = SL > 0;
+    const int L = CT ? SL : A.L, c = CT ? SC : A.c, d = CT ? SD : A.d, p = CT ? SP : A.p, q = CT ? SQ : A.q;
+    const int iM = CT ? SC * SQ : A.iM, iN = CT ? SQ * SD : A.iN;
+    const bool freq = A.B.branch == DGT_BRANCH_FREQ;
+    const int LQ = L / p * q;
+    const int LX = LQ > L ? LQ : L;
+    C* sF = (C*)smem_raw;        // L
+    C* sF2 = sF + L;             // L
+    C* sX = sF2 + L;             // max(L, LQ)
+    C* sY = sX + LX;             // max(L, LQ)
+    C* sG = sY + LX;             // L
+    C* sCh = sG + L;             // L
+    C* sTwL = sCh + L;           // L (F-branch)
+    C* sPh = sTwL + (freq ? L : 0);
+    unsigned int* sDst = (unsigned int*)(sPh + (freq ? LQ : 0));
+    C* sTwd = (C*)((char*)sPh + (freq ? (int64_t)LQ * sizeof(C) + (LQ + 1) / 2 * sizeof(C) : 0));
+    C* sTwm = sTwd + d;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int64_t w = blockIdx.x;
+    pdl_trigger();
+    {
+        const C* __restrict__ chirp = (const C*)A.chirp;
+        for (int i = tid; i < L; i += nt) {
+            sG[i] = __ldg((const C*)A.G + i);
+            sCh[i] = chirp ? __ldg(chirp + i) : mk<T>(T(1), T(0));
+            if (freq) sTwL[i] = __ldg((const C*)A.twL + i);
+        }
+        for (int i = tid; i < d; i += nt) sTwd[i] = __ldg((const C*)A.twd + i);
+        for (int i = tid; i < iM; i += nt) sTwm[i] = __ldg((const C*)A.twm + i);
+        if (freq && A.odst) {
+            for (int i = tid; i < LQ; i += nt) {
+                sPh[i] = __ldg((const C*)A.oph + i);
+                sDst[i] = __ldg((const unsigned int*)A.odst + i);
+            }
+        }
+    }
+    __syncthreads();
+    pdl_wait();
+    // ---- 7'. z(n, kc) into sX[n iM + kc] ----
+    const C* cw = (const C*)cin + w * A.B.M * A.B.N;
+    if (!freq) {
+        const C* __restrict__ E = (const C*)A.B.E;
+        const int Mi = (int)A.B.M, Ni = (int)A.B.N;
+        for (int i = tid; i < Mi * Ni; i += nt) {
+            const int n = i % Ni, mo = i / Ni;
+            int m = mo + __ldg(A.B.rot + n);
+            if (m >= Mi) m -= Mi;
+            const C v = cw[i];
+            sX[n * iM + m] = cmul(__ldg(E + n), mk<T>(v.x, -v.y));
+        }
+    } else {
+        for (int i = tid; i < LQ; i += nt) {
+            const C v = cw[sDst[i]];
+            sX[i] = cmul(sPh[i], mk<T>(v.x, -v.y));
+        }
+    }
+    __syncthreads();
+    // ---- 6'. DFT over kc of the iN columns ----
+    C* Z;
+    if constexpr (CT) {
+        tstage<T, 15, 15, 1>(sX, sY, iN, sTwm);
+        __syncthreads();
+        Z = sY;
+    } else {
+        Z = fft_smem<T>(sX, sY, A.rdm, iN, iM, sTwm);
+    }
+    C* R = Z == sX ? sY : sX;
+    // ---- 5'. gather rows (l, r, u) through the forward scatter map, DFT_d over tau ----
+    for (int i = tid; i < LQ; i += nt) {
+        const int np = i % d, t = i / d;          // row t = (l c + r) q + u, source n' of tau
+        const int u = t % q, lr = t / q;
+        const int r = lr % c, l = lr / c;
+        const int kappa = ((l - u) % q + q) % q;
+        const int off = l < u ? 1 : 0;
+        int tau = d - np - off;
+        if (tau >= d) tau -= d;
+        if (tau < 0) tau += d;
+        const int j = r + c * ((l * p) % q);
+        R[t * d + tau] = Z[(kappa + q * np) * iM + j];
+    }
+    __syncthreads();
+    C* Yd;
+    if constexpr (CT) {
+        tstage<T, 8, 8, 1>(R, Z, q * c * q, sTwd);
+        __syncthreads();
+        Yd = Z;
+    } else {
+        Yd = fft_smem<T>(R, Z, A.rdd, q * c * q, d, sTwd);
+    }
+    C* Acc = Yd == sX ? sY : sX;
+    // ---- 4'. acc(l, r, k; nu) = sum_u z(l, r, u; nu) G(r, u, k; nu) ----
+    for (int i = tid; i < L; i += nt) {
+        const int nu = i % d, t = i / d;          // t = (l c + r) p + k
+        const int k = t % p, lr = t / p;
+        const int r = lr % c;
+        C acc = mk<T>(T(0), T(0));
+        for (int u = 0; u < q; ++u)
+            acc = acc + cmul(Yd[(lr * q + u) * d + nu], sG[((r * q + u) * p + k) * d + nu]);
+        Acc[i] = acc;
+    }
+    __syncthreads();
+    // ---- 3'. DFT_d over nu ----
+    C* V;
+    if constexpr (CT) {
+        tstage<T, 8, 8, 1>(Acc, Yd, q * c * p, sTwd);
+        __syncthreads();
+        V = Yd;
+    } else {
+        V = fft_smem<T>(Acc, Yd, A.rdd, q * c * p, d, sTwd);
+    }
+    // ---- 2'. scatter through the Zak map with the chirp ----
+    {
+        const int Lc = L / c;
+        for (int i = tid; i < L; i += nt) {
+            const int s = i % d, t = i / d;
+            const int k = t % p, lr = t / p;
+            const int r = lr % c, l = lr / c;
+            const int x = r + c * ((k * q + p * l + s * p * q) % Lc);
+            sF[x] = cmul(sCh[x], V[i]);
+        }
+    }
+    __syncthreads();
+    // ---- 1'. F-branch DFT_L; f = conj(pre z) / conj(z) ----
+    const C* fz = sF;
+    if (freq) {
+        if constexpr (CT) {
+            tstage<T, 240, 16, 1>(sF, sF2, 1, sTwL);
+            __syncthreads();
+            tstage<T, 240, 15, 16>(sF2, sF, 1, sTwL);
+            __syncthreads();
+        } else {
+            fz = fft_smem<T>(sF, sF2, A.rdL, 1, L, sTwL);
+        }
+    }
+    const C* __restrict__ pre = (const C*)A.pre;
+    C* fo = (C*)fout + w * L;
+    for (int i = tid; i < L; i += nt) {
+        C v = fz[i];
+        if (pre) v = cmul(__ldg(pre + i), v);
+        fo[i] = mk<T>(v.x, -v.y);
+    }
+}

@@ -1,7 +1,7 @@
 """GPU parity of the one-CTA path (tiny.cuh: the whole shear algorithm of a short signal in one
-CTA; Alg. 1): every small lattice below is compared in full with the oracle (both
-branches, p > q and p < q, separable lambda, real input, both dtypes) and with the chunked
-kernels (NSDGT_TINY_OFF) of the same plan parameters."""
+CTA; Alg. 1, and its adjoint for the synthesis): every small lattice below is compared
+in full with the oracle's dgt / idgt (both branches, p > q and p < q, separable lambda, real
+input, both dtypes) and with the chunked kernels (NSDGT_TINY_OFF) of the same plan parameters."""
 import numpy as np
 import pytest
 
@@ -43,9 +43,17 @@ def test_tiny_vs_oracle_and_chunked(env, dtype, L, a, M, l1, l2, monkeypatch):
     assert [k["name"] for k in plan.profile_end()] == ["tiny"]
     assert plan.launches(2) == 1
     assert rel(c.cpu().numpy(), oracle.dgt(np.stack([f, f2]), g, a, M, l1, l2)) <= TOL[dtype]
+    # synthesis on the one-CTA path (tiny_adj_kernel) against the oracle's idgt
+    plan.profile_begin()
+    r = plan.inverse(c)
+    assert [k["name"] for k in plan.profile_end()] == ["tiny_adjoint"]
+    cn = c.cpu().numpy()
+    assert rel(r.cpu().numpy(), oracle.idgt(cn, g, a, M, l1, l2)) <= TOL[dtype]
     monkeypatch.setenv("NSDGT_TINY_OFF", "1")
-    c0 = nsdgt.Plan(L, a, M, l1, l2, g, dtype=dtype).execute(fb)
+    p0 = nsdgt.Plan(L, a, M, l1, l2, g, dtype=dtype)
+    c0 = p0.execute(fb)
     assert rel(c.cpu().numpy(), c0.cpu().numpy()) <= TOL[dtype]
+    assert rel(r.cpu().numpy(), p0.inverse(c).cpu().numpy()) <= TOL[dtype]
 
 
 def test_tiny_real_input_config1(env):
