@@ -22,14 +22,15 @@ def init(backend: str | None = None):
     import torch
     import torch.distributed as dist
     ws, rank, local = world()
+    # the rank's GPU first: NCCL binds its communicator to the current device
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     if ws > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         # NSDGT_DIST_BACKEND=gloo: functional runs of the N > 1 path with several ranks on one
         # GPU (NCCL refuses two ranks on one device); not for timing
         backend = backend or os.environ.get("NSDGT_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         dist.init_process_group(backend=backend)
-    if torch.cuda.is_available():
-        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     return ws, rank, local
 
 
