@@ -87,6 +87,15 @@ __global__ void k_chirp_table(cx<T>* out, int64_t sigma, int64_t L) {
     }
 }
 
+// out[s] = P_sigma(K s), s < n (the chirp's factor R of ZakArgs::chR)
+template <typename T>
+__global__ void k_chirp_stride(cx<T>* out, int64_t sigma, int64_t L, int64_t K, int64_t n) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = chirp_val(sigma, (K * s) % (2 * L), L);
+        out[s] = mk<T>((T)v.x, (T)v.y);
+    }
+}
+
 // gt = P_sigma * g  (fp64), g given in precision Tin
 template <typename Tin>
 __global__ void k_window_time(double2* gt, const cx<Tin>* g, int64_t sigma, int64_t L) {
@@ -277,6 +286,13 @@ struct ZakArgs {
     Radices rd;
     const void* tw;     // twiddles of length d
     int cnj;            // zak_ct only: intermediate stored [W][n][iM] (n = kappa + q n', j fastest)
+    // zak_ct only (chR non-null): the load chirp factorised on the gather's lattice x = x0 + K s
+    // (K = c q, x0 = r + c l, L = K d): P(x0 + K s) = P(x0) W_d^{-sigD x0 s} R(s), R(s) = P(K s),
+    // sigD = sigma (L + 1) mod d.  The gather multiplies R(s) (a d-entry table instead of the
+    // length-L one), and the W_d modulation is the index shift m0 = -sigD x0 (mod d) of the
+    // Zak DFT's output, applied with P(x0) where the products read it.
+    const void* chR;
+    int sigD;
 };
 
 template <typename T>
@@ -459,7 +475,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
                 v[it] = A.real_in ? mk<T>(fr[x], T(0)) : fc[x];
             }
         }
-        if (chirp) {
+        if (A.chR) {
+            const C* __restrict__ R = (const C*)A.chR;
+#pragma unroll
+            for (int it = 0; it < NG; ++it) {
+                const int i = tid + it * NT;
+                if (i < RBC * D) {
+                    const int rr = i % RBC, s = zrow<D, RBC, sizeof(C)>(i / RBC, rr, D);
+                    v[it] = cmul(v[it], __ldg(R + s));
+                }
+            }
+        } else if (chirp) {
 #pragma unroll
             for (int it = 0; it < NG; ++it) {
                 const int i = tid + it * NT;
@@ -492,10 +518,28 @@ __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_kernel(ZakArgs A) {
                 }
             }
         }
+        if (A.chR) {
+            // Phi(nu) = P(x0) U((nu + m0) mod D), U the DFT of f R (see ZakArgs::chR)
 #pragma unroll
-        for (int it = 0; it < NP; ++it) {
-            const int i = tid + it * NT;
-            if (i < Q * RBC * D) Yb[i] = cmul(phi[i % (RBC * D)], gv[it]);
+            for (int it = 0; it < NP; ++it) {
+                const int i = tid + it * NT;
+                if (i < Q * RBC * D) {
+                    const int rem = i % (RBC * D), rr = rem / D, nu = rem % D;
+                    const int x0 = r0 + rr + c * l;
+                    int m0 = D - (int)(((long long)A.sigD * x0) % D);
+                    if (m0 >= D) m0 -= D;
+                    int nn = nu + m0;
+                    if (nn >= D) nn -= D;
+                    const C P0 = __ldg(chirp + x0);
+                    Yb[i] = cmul(cmul(phi[rr * D + nn], P0), gv[it]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int it = 0; it < NP; ++it) {
+                const int i = tid + it * NT;
+                if (i < Q * RBC * D) Yb[i] = cmul(phi[i % (RBC * D)], gv[it]);
+            }
         }
     }
     __syncthreads();
@@ -1514,6 +1558,8 @@ struct Plan {
     int zrr = 0;             // forward Zak with zak_rr_kernel (d = 180 = 12 x 15 in registers)
     int front = 0;           // F-branch front end by front_f4096_kernel + zak_rr0_kernel (L = 180 x 4096)
     int outcl = 0;           // config 4: out_f4096 in clusters of 3 CTAs staging whole rows (k_cl_check)
+    void* chR = nullptr;     // zak_ct: the chirp's d-entry factor R(s) = P(c q s) (ZakArgs::chR)
+    int sigD = 0;
     int tiny = 0;            // whole transform of a signal in one CTA (tiny.cuh)
     unsigned int* tiny_dst = nullptr;   // F-branch output remap table (tiny.cuh)
     void* tiny_ph = nullptr;
@@ -1590,7 +1636,7 @@ static void free_plan(Plan* P) {
     if (P->inv_alias & 2) P->finv = nullptr;
     void* ptrs[] = {P->G, P->chirp, P->pre, P->tw_d, P->tw_m, P->E, P->rot, P->ptab, P->Cws, P->fhat,
                     P->stage_f[0], P->stage_f[1], P->stage_c[0], P->stage_c[1], P->Cinv, P->finv, P->gt64,
-                    P->scrA, P->scrB, P->twL, P->tiny_dst, P->tiny_ph, P->tiny_pack};
+                    P->scrA, P->scrB, P->twL, P->tiny_dst, P->tiny_ph, P->tiny_pack, P->chR};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     free_fast(&P->fp);
@@ -1689,6 +1735,15 @@ static int build_tables(Plan* P, const void* g_in, bool g_host, cudaStream_t st)
     if (I.chirp_sigma % (2 * L) != 0) {
         CUDA_TRY(cudaMalloc(&P->chirp, sizeof(C) * L));
         k_chirp_table<T><<<grid_for(L), 256, 0, st>>>((C*)P->chirp, I.chirp_sigma, L);
+    }
+    // zak_ct (p = 1, compile-time d): the chirp factorised on the gather lattice (ZakArgs::chR);
+    // NSDGT_CHR_OFF keeps the length-L table on the load
+    if (P->chirp && P->zct && I.p == 1 && !std::getenv("NSDGT_CHR_OFF")) {
+        CUDA_TRY(cudaMalloc(&P->chR, sizeof(C) * I.d));
+        k_chirp_stride<T><<<grid_for(I.d), 256, 0, st>>>((C*)P->chR, I.chirp_sigma, L, I.c * I.q, I.d);
+        const int64_t D = I.d;
+        const int64_t sg = ((I.chirp_sigma % (2 * L)) + 2 * L) % (2 * L);
+        P->sigD = (int)(((sg % D) * ((L + 1) % D)) % D);
     }
     if (I.branch == DGT_BRANCH_FREQ && I.pre_sigma % (2 * L) != 0) {
         CUDA_TRY(cudaMalloc(&P->pre, sizeof(C) * L));
@@ -1863,6 +1918,7 @@ static int launch_chunk(Plan* P, const void* f, void* c, int64_t Wc, cudaStream_
     }
     ZakArgs A{};
     A.f = src; A.real_in = real_src; A.chirp = P->chirp; A.G = P->G; A.C = P->Cws;
+    A.chR = P->chR; A.sigD = P->sigD;
     A.L = I.L; A.c = I.c; A.d = I.d; A.p = I.p; A.q = I.q; A.iM = I.iM;
     A.RB = P->RB; A.rd = P->rd_d; A.tw = P->tw_d; A.allu = P->allu; A.cnj = P->cnj;
     A.gscr = P->gA ? P->scrA : nullptr; A.gstride = (int64_t)std::max(P->smemA, P->smemAinv);

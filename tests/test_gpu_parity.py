@@ -593,3 +593,22 @@ def test_config4_cluster_output_variant(torch_cuda, nsdgt, monkeypatch):
     monkeypatch.setenv("NSDGT_OUTCL", "1")
     c1 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c128").execute(f)
     assert torch.equal(c0, c1)
+
+
+def test_factorised_chirp_matches_table(torch_cuda, nsdgt, monkeypatch):
+    """zak_ct multiplies the load chirp as P(x0) W_d^{-sigD x0 s} R(s) (a d-entry table and an
+    index shift of the Zak DFT's output, ZakArgs::chR) instead of the length-L table
+    (NSDGT_CHR_OFF): config 2's lattice and config 4's lattice on the zak_ct path agree."""
+    torch = torch_cuda
+    for k in (2, 4):
+        wl = CONFIGS[k - 1]
+        g = window(wl)
+        f = torch.from_numpy(batch(wl, 0, 1)).cuda()
+        if k == 4:
+            monkeypatch.setenv("NSDGT_FRONT_CUFFT", "1")
+            monkeypatch.setenv("NSDGT_ZAK_CT", "1")
+        c1 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c128").execute(f)
+        monkeypatch.setenv("NSDGT_CHR_OFF", "1")
+        c0 = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, g, dtype="c128").execute(f)
+        monkeypatch.delenv("NSDGT_CHR_OFF")
+        assert rel(c1.cpu().numpy(), c0.cpu().numpy()) <= 1e-12, k
