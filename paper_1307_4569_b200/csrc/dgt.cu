@@ -787,25 +787,28 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
     const C* __restrict__ Cin = (const C*)A.C + w * iM * iN;
     // load columns: C(j, n) stored at [j][n mod q][n div q] (32-bit indices within a signal);
     // eight independent loads in flight per thread
-    if (IMCT > 0 && nt == 16 && qi == 4 && ns == 1 && (nb & 3) == 0) {
-        // config 2 (M' = 200, q = 4, 16 consecutive columns = 4 kappa x 4 n'): element
-        // i = (j, kappa, n'') with n'' fastest, so 4 lanes read 64 contiguous bytes of row
-        // (j, kappa); every index by shifts (the generic loop divides by runtime nt and q)
-        const int nq0 = (int)nb >> 2;
-        constexpr int U = (16 * (IMCT > 0 ? IMCT : 1) + 255) / 256;
+    if (IMCT > 0 && (nt == 16 || nt == 20) && qi == 4 && ns == 1 && (nb & 3) == 0) {
+        // config 2 (M' = 200, q = 4, nt consecutive columns = 4 kappa x nt/4 n'): element
+        // i = (j, kappa, n'') with n'' fastest, so nt/4 lanes read contiguous bytes of row
+        // (j, kappa) (the generic loop's lanes each touch another row)
+        const int nq0 = (int)nb >> 2, NQ = nt >> 2;
+        constexpr int U = (20 * (IMCT > 0 ? IMCT : 1) + 255) / 256;
         C v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = threadIdx.x + 256 * u;
-            if (i < 16 * iMi) {
-                const int nn = i & 3, kap = (i >> 2) & 3, j = i >> 4;
+            if (i < nt * iMi) {
+                const int t = i / NQ, nn = i - t * NQ, kap = t & 3, j = t >> 2;
                 v[u] = Cin[(j * 4 + kap) * di + nq0 + nn];
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = threadIdx.x + 256 * u;
-            if (i < 16 * iMi) bufA[(4 * (i & 3) + ((i >> 2) & 3)) * iMi + (i >> 4)] = v[u];   // column cl = 4 n'' + kappa
+            if (i < nt * iMi) {
+                const int t = i / NQ, nn = i - t * NQ;
+                bufA[(4 * nn + (t & 3)) * iMi + (t >> 2)] = v[u];   // column cl = 4 n'' + kappa
+            }
         }
     } else {
         const int total = nt * iMi, nbi = (int)nb, nsi = (int)ns;
