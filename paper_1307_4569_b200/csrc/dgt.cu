@@ -993,6 +993,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) out_adj_kernel(OutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
+    pdl_trigger();
+    pdl_wait();
     const int64_t iM = A.iM, iN = A.iN, q = A.q, d = A.d;
     const int NT = A.NT;
     const int iMi = (int)iM, qi = (int)q, di = (int)d;
@@ -1108,6 +1110,8 @@ template <typename T, int MINB>
 __global__ void __launch_bounds__(256, MINB) out_f4096_adj_kernel(OutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
+    pdl_trigger();
+    pdl_wait();
     C* S = (C*)smem_raw;
     const int tid = threadIdx.x;
     const int m = blockIdx.x;
@@ -1147,6 +1151,8 @@ template <typename T, int D, int Q, int RBC, int NT = 256>
 __global__ void __launch_bounds__(NT, 512 / NT) zak_ct_adj_kernel(ZakArgs A, void* fout) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
+    pdl_trigger();
+    pdl_wait();
     constexpr int NG = (RBC * D + NT - 1) / NT, NP = (Q * RBC * D + NT - 1) / NT;
     const int c = (int)A.c;
     const int nrb = c / RBC;
@@ -1232,6 +1238,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) zak_adj_kernel(ZakArgs A, void* fout) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
+    pdl_trigger();
+    pdl_wait();
     const int64_t d = A.d, p = A.p, q = A.q, c = A.c, L = A.L;
     const int RB = A.RB;
     const int nrb = (int)((c + RB - 1) / RB);
@@ -2220,11 +2228,13 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
     const int ntiles = B.grouped ? (int)(I.q * ((I.d + P->NT - 1) / P->NT)) : (int)((I.iN + P->NT - 1) / P->NT);
     int ph = prof_open(P, st);
     if (P->outk == 2)
-        out_f4096_adj_kernel<T, 2><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+        CUDA_TRY(launch_pdl(out_f4096_adj_kernel<T, 2>, dim3((unsigned)I.iN, (unsigned)Wc), dim3(256),
+                            kOutF4096Elems * sizeof(C), st, B));
     else if (P->outk == 1)
-        out_f4096_adj_kernel<T, 3><<<dim3((unsigned)I.iN, (unsigned)Wc), 256, kOutF4096Elems * sizeof(C), st>>>(B);
+        CUDA_TRY(launch_pdl(out_f4096_adj_kernel<T, 3>, dim3((unsigned)I.iN, (unsigned)Wc), dim3(256),
+                            kOutF4096Elems * sizeof(C), st, B));
     else
-        out_adj_kernel<T><<<dim3(ntiles, (unsigned)Wc), 256, P->gB ? 0 : P->smemB, st>>>(B);
+        CUDA_TRY(launch_pdl(out_adj_kernel<T>, dim3(ntiles, (unsigned)Wc), dim3(256), P->gB ? 0 : P->smemB, st, B));
     prof_close(P, ph, PK_OUTADJ, Wc * MN * e, Wc * (4.0 * MN * std::log2((double)I.iM) + 6.0 * MN), st);
     ZakArgs A{};
     A.f = nullptr; A.real_in = 0; A.chirp = P->chirp; A.G = P->G; A.C = P->Cinv;
@@ -2240,13 +2250,17 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
         CUDA_TRY(launch_pdl(zak_rr0_adj_kernel<T, 8, kZrr0MinB>, dim3((unsigned)(I.c / 8 * I.q), (unsigned)Wc),
                             dim3(128), zrr_smem<T>(), st, A, zout));
     else if (P->zct == 180 && sizeof(C) == 16)
-        zak_ct_adj_kernel<T, 180, 4, 4><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
+        CUDA_TRY(launch_pdl(zak_ct_adj_kernel<T, 180, 4, 4>, dim3(nrb * (unsigned)I.q, (unsigned)Wc), dim3(256), P->smemA,
+                            st, A, zout));
     else if (P->zct == 180)
-        zak_ct_adj_kernel<T, 180, 4, 8><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
+        CUDA_TRY(launch_pdl(zak_ct_adj_kernel<T, 180, 4, 8>, dim3(nrb * (unsigned)I.q, (unsigned)Wc), dim3(256), P->smemA,
+                            st, A, zout));
     else if (P->zct == 720)
-        zak_ct_adj_kernel<T, 720, 4, 1><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->smemA, st>>>(A, zout);
+        CUDA_TRY(launch_pdl(zak_ct_adj_kernel<T, 720, 4, 1>, dim3(nrb * (unsigned)I.q, (unsigned)Wc), dim3(256), P->smemA,
+                            st, A, zout));
     else
-        zak_adj_kernel<T><<<dim3(nrb * (unsigned)I.q, (unsigned)Wc), 256, P->gA ? 0 : P->smemAinv, st>>>(A, zout);
+        CUDA_TRY(launch_pdl(zak_adj_kernel<T>, dim3(nrb * (unsigned)I.q, (unsigned)Wc), dim3(256),
+                            P->gA ? 0 : P->smemAinv, st, A, zout));
     prof_close(P, ph, PK_ZAKADJ, Wc * L * e + L * e, Wc * (8.0 * L * I.q / I.p + 4.0 * L * lg_d + 4.0 * MN * lg_d), st);
     CUDA_TRY(cudaGetLastError());
     return DGT_OK;
