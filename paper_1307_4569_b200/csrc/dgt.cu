@@ -989,7 +989,7 @@ __global__ void k_cl_check(OutArgs A, int* bad) {
 //   T-branch: X'(m', n) = conj(E(n)) c[(m' - rot(n)) mod M][n];  F-branch: X'(kc, m) =
 //   conj(E(k,m)) c[kt][mt] (the Alg. 1 remap read backwards);  then C'(j, n) = sum_m' X'(m', n)
 //   exp(+2 pi i j m' / iM).
-template <typename T>
+template <typename T, int IMCT = 0>   // IMCT = 200: the compile-time DFT over m (config 2)
 __global__ void __launch_bounds__(256) out_adj_kernel(OutArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using C = cx<T>;
@@ -1060,9 +1060,22 @@ __global__ void __launch_bounds__(256) out_adj_kernel(OutArgs A) {
         }
     }
     __syncthreads();
-    C* X = fft_smem<T>(bufA, bufB, A.rd, nt, iMi, (const C*)A.tw);
+    C* X;
+    if constexpr (IMCT > 0) X = fft_ct<T, IMCT>(bufA, bufB, nt, (const C*)A.tw);
+    else X = fft_smem<T>(bufA, bufB, A.rd, nt, iMi, (const C*)A.tw);
     // C'(j, n) = conj(X(j)), stored at [j][n mod q][n div q]
     C* Cw = (C*)A.C + w * iM * iN;
+    if (IMCT > 0 && (nt == 16 || nt == 20) && qi == 4 && ns == 1 && (nb & 3) == 0) {
+        // config 2: element i = (j, kappa, n'') with n'' fastest -- nt/4 lanes store contiguous
+        // bytes of row (j, kappa) (the generic loop's lanes each hit another row)
+        const int nq0 = (int)nb >> 2, NQ = nt >> 2;
+        for (int i = threadIdx.x; i < nt * iMi; i += blockDim.x) {
+            const int t = i / NQ, nn = i - t * NQ, kap = t & 3, j = t >> 2;
+            const C v = X[(4 * nn + kap) * iMi + j];
+            Cw[(j * 4 + kap) * di + nq0 + nn] = mk<T>(v.x, -v.y);
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < nt * iMi; i += blockDim.x) {
         const int cl = i % nt, j = i / nt;
         const int n = (int)(nb + ns * cl);
@@ -2132,6 +2145,8 @@ static int configure(Plan* P, int64_t max_chunk) {
     P->smemAinv = (size_t)P->RB * (2 * I.p + 1) * I.d * e;
     CUDA_TRY(cudaFuncSetAttribute(zak_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gA ? 0 : (int)P->smemAinv));
     CUDA_TRY(cudaFuncSetAttribute(out_adj_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, P->gB ? 0 : (int)P->smemB));
+    if (P->outct == 200)
+        CUDA_TRY(cudaFuncSetAttribute(out_adj_kernel<T, 200>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemB));
     if (P->zct) {
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 180, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
         CUDA_TRY(cudaFuncSetAttribute(zak_ct_adj_kernel<T, 180, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smemA));
@@ -2234,7 +2249,8 @@ static int launch_inverse_chunk(Plan* P, const void* c, void* f, int64_t Wc, cud
         CUDA_TRY(launch_pdl(out_f4096_adj_kernel<T, 3>, dim3((unsigned)I.iN, (unsigned)Wc), dim3(256),
                             kOutF4096Elems * sizeof(C), st, B));
     else
-        CUDA_TRY(launch_pdl(out_adj_kernel<T>, dim3(ntiles, (unsigned)Wc), dim3(256), P->gB ? 0 : P->smemB, st, B));
+        CUDA_TRY(P->outct == 200 ? launch_pdl(out_adj_kernel<T, 200>, dim3(ntiles, (unsigned)Wc), dim3(256), P->smemB, st, B)
+                                 : launch_pdl(out_adj_kernel<T>, dim3(ntiles, (unsigned)Wc), dim3(256), P->gB ? 0 : P->smemB, st, B));
     prof_close(P, ph, PK_OUTADJ, Wc * MN * e, Wc * (4.0 * MN * std::log2((double)I.iM) + 6.0 * MN), st);
     ZakArgs A{};
     A.f = nullptr; A.real_in = 0; A.chirp = P->chirp; A.G = P->G; A.C = P->Cinv;
