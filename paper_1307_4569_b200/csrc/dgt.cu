@@ -774,7 +774,10 @@ __global__ void __launch_bounds__(256) out_kernel(OutArgs A) {
     KTRACE(10);
     C Et = mk<T>(T(1), T(0));
     int rott = 0;
-    const bool colfix = A.branch != DGT_BRANCH_FREQ && nt > 0 && 256 % nt == 0;
+#ifndef NSDGT_OUT_COLFIX   // experiment builds: 0 reads E(n), rot(n) per element (config 2: 33.6 vs 31.8 us)
+#define NSDGT_OUT_COLFIX 1
+#endif
+    const bool colfix = NSDGT_OUT_COLFIX && A.branch != DGT_BRANCH_FREQ && nt > 0 && 256 % nt == 0;
     if (colfix) {
         const int n = (int)nb + (int)(threadIdx.x % nt);
         Et = __ldg((const C*)A.E + n);
