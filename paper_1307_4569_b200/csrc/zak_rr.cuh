@@ -14,10 +14,16 @@
 //     registers (its inputs are exactly the Phi it holds -- no exchange between the DFTs),
 //     one exchange, the "t2-thread" runs DFT_15 and scatters to the intermediate directly.
 //
-// Shared memory carries 3 exchanges per u-pair instead of the Stockham engine's 2 passes per
-// DFT plus the gather / product / scatter round trips (10 vs 33 transfers of a 180-vector per
-// column), and 5 barriers per CTA instead of 13.  RBC consecutive residues per CTA (rr fastest
-// in every thread mapping: 16 * RBC-byte runs in global memory, conflict-free exchanges).
+// Shared memory carries one exchange per DFT (5 per column: 10 transfers of a 180-vector
+// against 33 for the Stockham engine's two passes per DFT plus the gather / product / scatter
+// round trips) and 5 barriers per CTA instead of 13.  RBC consecutive residues per CTA (rr
+// fastest in every thread mapping: 16 * RBC-byte runs in global memory, conflict-free
+// exchanges).
+//
+// Also here: front_f4096_kernel (the frequency shear's length-L FFT for L = 180 x 4096 as
+// 4096-point DFTs of the 180 residues; its adjoint with ADJ), zak_rr0_kernel (zak_rr with the
+// FFT's DFT_180 over the residues in front: six DFT_180s per column, still one exchange each)
+// and zak_rr0_adj_kernel (the adjoint of zak_rr0, for the synthesis).
 // Included inside namespace nsdgt by dgt.cu, after ZakArgs.
 #pragma once
 
