@@ -130,3 +130,25 @@ def test_new_paths_bitwise_deterministic(env):
         for _ in range(4):
             assert torch.equal(plan.execute(f), c0), wl.name
             assert torch.equal(plan.inverse(c0), r0), wl.name
+
+
+@pytest.mark.parametrize("cfg", [0, 3])
+def test_empty_batches_on_new_paths(env, cfg):
+    """W = 0 on the one-CTA path (config 1) and on config 4's front path: forward, synthesis
+    and the host path launch nothing and return empty results; a ragged batch (W not a multiple
+    of the front batch / chunk) still matches signal-by-signal runs."""
+    torch, nsdgt, oracle = env
+    wl = CONFIGS[cfg]
+    plan = nsdgt.Plan(wl.L, wl.a, wl.M, wl.lam1, wl.lam2, window(wl), dtype=wl.dtype, real_input=wl.real_input)
+    fdt = torch.float64 if wl.real_input else (torch.complex64 if wl.dtype == "c64" else torch.complex128)
+    cdt = torch.complex64 if wl.dtype == "c64" else torch.complex128
+    assert plan.launches(0) == 0
+    e = plan.execute(torch.empty((0, wl.L), dtype=fdt, device="cuda"))
+    assert e.shape == (0, wl.M, wl.N)
+    r = plan.inverse(torch.empty((0, wl.M, wl.N), dtype=cdt, device="cuda"))
+    assert r.shape[0] == 0
+    W = 3 if cfg == 0 else 2
+    f = torch.from_numpy(batch(wl, 0, W)).cuda()
+    c = plan.execute(f)
+    for w in range(W):
+        assert torch.equal(c[w], plan.execute(f[w:w + 1])[0])
